@@ -1,0 +1,156 @@
+/*
+ * genoiht_cuda.h -- C ABI of libgenoiht_cuda.so, the sm_100a (B200) drop-in for
+ * the IHT hot path of the reference package genoiht 0.1.0
+ * (/root/reference/pkg/src/genoiht; arXiv 1608.01398 re-implementation).
+ *
+ * Conventions
+ *   - Every function returns 0 on success and -1 on failure; gi_last_error()
+ *     returns a thread-local message for the failing call.
+ *   - Plain pointers and sizes only.  "Host" arguments are borrowed for the
+ *     duration of the call; outputs are caller-allocated, as with the
+ *     reference's numba kernels (geno_matrix.py:334, :361, :369).
+ *   - gi_matrix handles own device memory.  A handle may be shared by several
+ *     host threads: host-buffer calls serialise on a per-handle mutex, like the
+ *     reference's _KERNEL_LOCK (geno_matrix.py:58-61); results never depend on
+ *     which thread calls.
+ *   - gi_dev_* functions take DEVICE pointers (on the handle's device) and a
+ *     CUDA stream (cudaStream_t passed as void*, NULL = legacy default stream);
+ *     they only enqueue work.  They are the building blocks of the device IHT
+ *     loop (paper_1608_01398_b200/iht.py) and hold no hidden state, so any
+ *     number of fits may run concurrently on one matrix.
+ *   - Genotype bytes use the reference's BED layout on the host side:
+ *     variant-major uint8[p, ceil(n/4)], four samples per byte from the least
+ *     significant bit pair, codes 00 -> 0, 01 -> missing, 10 -> 1, 11 -> 2
+ *     (plink_io.py:3-15).  On the device they live in the swizzled sample-tile
+ *     layout described in paper_1608_01398_b200/csrc/common.cuh.
+ */
+#ifndef GENOIHT_CUDA_H
+#define GENOIHT_CUDA_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gi_matrix gi_matrix;
+
+/* ---------------------------------------------------------------- runtime */
+int gi_version(void);
+const char *gi_last_error(void);
+/* number of visible CUDA devices (0 when none) */
+int gi_device_count(int *count);
+/* SM count, total HBM bytes and L2 bytes of a device */
+int gi_device_info(int device, int *sm_count, int64_t *mem_bytes, int64_t *l2_bytes);
+/* cudaDeviceSynchronize on `device` (used by timing code) */
+int gi_device_sync(int device);
+
+/* ---------------------------------------------------------- construction */
+/* Replaces PackedGenotypeMatrix.from_bed_buffer (geno_matrix.py:281-292) and
+ * _packed_stats (:239-246): uploads `data` (host, variant-major p x ceil(n/4),
+ * kept verbatim) to `device` and computes u, v bit-identically. */
+int gi_matrix_from_bed(const uint8_t *data, int64_t n, int64_t p, int device, gi_matrix **out);
+/* Device-side synthetic genotypes with the law of random_packed_matrix
+ * (simulate.py:56-65) from a counter-based stream; SNP j_base + j of the
+ * unsharded matrix gets identical bytes in any shard.  CPU twin: oracle/. */
+int gi_matrix_synth(uint64_t seed, int64_t n, int64_t p, int64_t j_base, double maf_lo,
+                    double maf_hi, double missing, int device, gi_matrix **out);
+/* Replaces PackedGenotypeMatrix.with_stats (geno_matrix.py:310-316): new handle
+ * sharing the packed bytes, with caller stats (host arrays of length p). */
+int gi_matrix_with_stats(const gi_matrix *h, const double *u, const double *v, gi_matrix **out);
+/* Replaces PackedGenotypeMatrix.subset_rows (geno_matrix.py:305-308): rows are
+ * gathered on the device into a new matrix whose u, v are recomputed. */
+int gi_matrix_subset_rows(const gi_matrix *h, const int64_t *rows, int64_t m, gi_matrix **out);
+int gi_matrix_free(gi_matrix *h);
+
+/* ------------------------------------------------------------ inspection */
+int gi_matrix_shape(const gi_matrix *h, int64_t *n, int64_t *p, int *device);
+/* u, v (host out, length p): PackedGenotypeMatrix.u / .v */
+int gi_matrix_stats(const gi_matrix *h, double *u, double *v);
+/* BED bytes of SNPs [j0, j0 + count) (host out, count x ceil(n/4)); backs
+ * PackedGenotypeMatrix.data, to_codes (:294-296) and write_bed (plink_io.py:103-112) */
+int gi_matrix_read_bed(const gi_matrix *h, int64_t j0, int64_t count, uint8_t *out);
+/* per-SNP count of missing genotypes (host out, length p) */
+int gi_matrix_missing_counts(const gi_matrix *h, int32_t *out);
+/* device pointers of the handle's u and v (length p) */
+int gi_matrix_device_stats(const gi_matrix *h, const double **d_u, const double **d_v);
+/* column statistics over the rows with keep[i] != 0 (host in, length n):
+ * the u, v that subset_rows(rows) would compute, without re-packing */
+int gi_matrix_masked_stats(const gi_matrix *h, const uint8_t *keep, double *u, double *v);
+
+/* ------------------------------------------------ operator protocol (host) */
+/* aty_genetic (geno_matrix.py:351-364).  mode 0: exact -- bit-identical to
+ * _aty_kernel (:142-165) when sum_r is numpy's r.sum(); mode 1: fast lookup-
+ * table kernel (fp32 tables, fp64 accumulation; sum_r ignored). */
+int gi_aty(gi_matrix *h, const double *r, double sum_r, double *out, int mode);
+/* ax_columns (geno_matrix.py:328-349), bit-identical to _ax_cols_kernel (:168-194) */
+int gi_ax_cols(gi_matrix *h, const int64_t *idx, const double *w, int64_t k, double *out);
+/* decompress (geno_matrix.py:366-373): out_t is (k, n) row-major, i.e. the
+ * reference's out_t before its final transpose; bit-identical to :216-236 */
+int gi_decompress(gi_matrix *h, const int64_t *idx, int64_t k, double *out_t);
+
+/* ------------------------------------------- device primitives (IHT loop) */
+/* u, v may be NULL to use the handle's own statistics. */
+int gi_dev_ax(gi_matrix *h, const double *u, const double *v, const int64_t *d_idx,
+              const double *d_w, int64_t k, double *d_out, int accumulate, void *stream);
+/* g = scale * X^T r with the lookup-table kernel; d_rt is fp32(r - mean) padded
+ * to gi_padded_samples(h) entries, d_sum_rt a device scalar (sum of d_rt). */
+int gi_dev_aty_fast(gi_matrix *h, const double *u, const double *v, const float *d_rt,
+                    const double *d_sum_rt, double scale, double *d_out, void *stream);
+/* exact kernel: d_rpad fp64 padded to gi_padded_samples(h), d_sum_r device scalar */
+int gi_dev_aty_exact(gi_matrix *h, const double *u, const double *v, const double *d_rpad,
+                     const double *d_sum_r, double scale, double *d_out, void *stream);
+int64_t gi_padded_samples(const gi_matrix *h);
+/* masked column statistics into device arrays; d_rowmask has one uint32 per
+ * (tile, word) = gi_padded_samples/16 entries, bit 2s set for included sample s */
+int gi_dev_stats(gi_matrix *h, const uint32_t *d_rowmask, double *d_u, double *d_v,
+                 void *stream);
+
+/* Reduction workspace: d_partials >= gi_red_partials() doubles, d_ticket one
+ * zero-initialised uint32 (the kernels leave it zero again). */
+int64_t gi_red_partials(void);
+/* r = keep ? y - (fit + C bcov) : 0; d_scal[0] = 0.5 r.r, d_scal[1] = sum(r)/n_eff.
+ * d_fit, d_C, d_keep may be NULL; C is row-major (n, c). */
+int gi_dev_residual(int64_t n, const double *d_y, const double *d_fit, const double *d_C,
+                    int64_t c, const double *d_bcov, const uint8_t *d_keep, double n_eff,
+                    double *d_r, double *d_scal, double *d_partials, uint32_t *d_ticket,
+                    void *stream);
+/* rt = keep ? fp32(r - d_scal[1]) : 0 over n_pad entries; d_scal[2] = sum(rt) */
+int gi_dev_center(int64_t n, int64_t n_pad, const double *d_r, const uint8_t *d_keep,
+                  double *d_scal, float *d_rt, double *d_partials, uint32_t *d_ticket,
+                  void *stream);
+/* d_gcov[l] = -sum_i C[i, l] r_i, l < c <= 8 */
+int gi_dev_covgrad(int64_t n, const double *d_C, int64_t c, const double *d_r, double *d_gcov,
+                   double *d_partials, uint32_t *d_ticket, void *stream);
+/* d_scal[slot] = max |x| */
+int gi_dev_maxabs(int64_t m, const double *d_x, double *d_scal, int slot, double *d_partials,
+                  uint32_t *d_ticket, void *stream);
+/* d_scal[slot] = x . x */
+int gi_dev_sumsq(int64_t m, const double *d_x, double *d_scal, int slot, double *d_partials,
+                 uint32_t *d_ticket, void *stream);
+/* x += C w (C row-major (n, c)) */
+int gi_dev_add_cov(int64_t n, const double *d_C, int64_t c, const double *d_w, double *d_x,
+                   void *stream);
+
+/* Hard-threshold select (top_k_indices iht.py:36-49, hard_threshold :52-58):
+ * the k largest |value| under (|value| desc, index asc), value = g_j (mode 0)
+ * or beta_j - mu * g_j (mode 1, computed with the reference's two roundings).
+ * Candidate scratch: gi_topk_slots(p, k) entries each of d_ckey/d_cidx/d_cval.
+ * Outputs (unordered, *d_count <= k): global index (idx_base + local j),
+ * value, key (|value| bits + 1). */
+int64_t gi_topk_slots(int64_t p, int64_t k);
+int gi_dev_topk(int64_t p, int64_t k, int mode, const double *d_beta, const double *d_g,
+                double mu, int64_t idx_base, uint64_t *d_ckey, int64_t *d_cidx, double *d_cval,
+                int64_t *d_out_idx, double *d_out_val, uint64_t *d_out_key, int64_t *d_count,
+                void *stream);
+/* beta[idx[t]] = val[t];  dst[t] = src[idx[t]] */
+int gi_dev_scatter(int64_t k, const int64_t *d_idx, const double *d_val, double *d_beta,
+                   void *stream);
+int gi_dev_gather(int64_t k, const int64_t *d_idx, const double *d_src, double *d_dst,
+                  void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GENOIHT_CUDA_H */

@@ -1,0 +1,127 @@
+"""ctypes binding of libgenoiht_cuda.so (include/genoiht_cuda.h).
+
+The library is the product's only compute path.  It is built in-tree by
+``__graft_entry__.build()`` (``make -C paper_1608_01398_b200/csrc``); there is
+no CPU fallback: if the shared object or a CUDA device is missing, every entry
+point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgenoiht_cuda.so")
+
+_lib = None
+_lock = threading.Lock()
+
+c_i64 = ctypes.c_int64
+c_int = ctypes.c_int
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+c_u64 = ctypes.c_uint64
+
+
+class NativeError(RuntimeError):
+    """A CUDA-side failure reported through gi_last_error()."""
+
+
+def _declare(lib):
+    P = c_vp
+    sig = {
+        "gi_version": ([], c_int),
+        "gi_last_error": ([], ctypes.c_char_p),
+        "gi_device_count": ([P], c_int),
+        "gi_device_info": ([c_int, P, P, P], c_int),
+        "gi_device_sync": ([c_int], c_int),
+        "gi_matrix_from_bed": ([P, c_i64, c_i64, c_int, P], c_int),
+        "gi_matrix_synth": ([c_u64, c_i64, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_int, P], c_int),
+        "gi_matrix_with_stats": ([P, P, P, P], c_int),
+        "gi_matrix_subset_rows": ([P, P, c_i64, P], c_int),
+        "gi_matrix_free": ([P], c_int),
+        "gi_matrix_shape": ([P, P, P, P], c_int),
+        "gi_matrix_stats": ([P, P, P], c_int),
+        "gi_matrix_read_bed": ([P, c_i64, c_i64, P], c_int),
+        "gi_matrix_missing_counts": ([P, P], c_int),
+        "gi_matrix_device_stats": ([P, P, P], c_int),
+        "gi_matrix_masked_stats": ([P, P, P, P], c_int),
+        "gi_aty": ([P, P, c_dbl, P, c_int], c_int),
+        "gi_ax_cols": ([P, P, P, c_i64, P], c_int),
+        "gi_decompress": ([P, P, c_i64, P], c_int),
+        "gi_dev_ax": ([P, P, P, P, P, c_i64, P, c_int, P], c_int),
+        "gi_dev_aty_fast": ([P, P, P, P, P, c_dbl, P, P], c_int),
+        "gi_dev_aty_exact": ([P, P, P, P, P, c_dbl, P, P], c_int),
+        "gi_padded_samples": ([P], c_i64),
+        "gi_dev_stats": ([P, P, P, P, P], c_int),
+        "gi_red_partials": ([], c_i64),
+        "gi_dev_residual": ([c_i64, P, P, P, c_i64, P, P, c_dbl, P, P, P, P, P], c_int),
+        "gi_dev_center": ([c_i64, c_i64, P, P, P, P, P, P, P], c_int),
+        "gi_dev_covgrad": ([c_i64, P, c_i64, P, P, P, P, P], c_int),
+        "gi_dev_maxabs": ([c_i64, P, P, c_int, P, P, P], c_int),
+        "gi_dev_sumsq": ([c_i64, P, P, c_int, P, P, P], c_int),
+        "gi_dev_add_cov": ([c_i64, P, c_i64, P, P, P], c_int),
+        "gi_topk_slots": ([c_i64, c_i64], c_i64),
+        "gi_dev_topk": ([c_i64, c_i64, c_int, P, P, c_dbl, c_i64, P, P, P, P, P, P, P, P], c_int),
+        "gi_dev_scatter": ([c_i64, P, P, P, P], c_int),
+        "gi_dev_gather": ([c_i64, P, P, P, P], c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def lib():
+    """The loaded library; raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise NativeError(
+                        f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                        "(there is no CPU fallback)")
+                h = ctypes.CDLL(LIB_PATH)
+                _declare(h)
+                _lib = h
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().gi_last_error()
+        raise NativeError(msg.decode() if msg else "unknown CUDA failure")
+
+
+def device_count() -> int:
+    out = c_int(0)
+    check(lib().gi_device_count(ctypes.byref(out)))
+    return int(out.value)
+
+
+def require_device(device: int = 0) -> None:
+    count = device_count()
+    if count == 0:
+        raise NativeError("no CUDA device is visible; the genoiht B200 path has no CPU fallback")
+    if not 0 <= device < count:
+        raise NativeError(f"CUDA device {device} out of range (0..{count - 1})")
+
+
+def device_info(device: int = 0):
+    sms = c_int(0)
+    mem = c_i64(0)
+    l2 = c_i64(0)
+    check(lib().gi_device_info(device, ctypes.byref(sms), ctypes.byref(mem), ctypes.byref(l2)))
+    return int(sms.value), int(mem.value), int(l2.value)
+
+
+def ptr(array) -> int:
+    """Address of a numpy array, torch tensor or None."""
+    if array is None:
+        return None
+    if hasattr(array, "data_ptr"):
+        return array.data_ptr()
+    return array.ctypes.data

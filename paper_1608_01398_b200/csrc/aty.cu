@@ -1,0 +1,499 @@
+// X^T r over the swizzled packed-genotype tiles (the north-star kernel).
+//
+// Reference: _aty_kernel geno_matrix.py:142-165, reached through
+// PackedGenotypeMatrix.aty_genetic :351-364 and aty :570-575.
+//   out_j = scale * v_j * (t_j - u_j * (sum_r - m_j)),
+//   t_j = sum_i dose_ij r_i,  m_j = sum_{i missing} r_i.
+//
+// Two kernels:
+//
+// aty_fast_kernel  (the IHT loop's gradient; HBM-bound target)
+//   Per 512-sample tile the CTA builds a lookup table in shared memory,
+//     T[pos][b] = sum_{s<4} dose(code_s(b)) * rt[4 pos + s]        (fp32)
+//   for every byte value b at each of the 128 byte positions (128 KiB), where
+//   rt = fp32(r - mean(r)) is the centred residual.  Each packed byte then
+//   costs one PRMT (byte -> table address), one LDS and one FADD: 0.75
+//   instructions per genotype, no decode arithmetic.  Lane L owns SNP L of a
+//   32-SNP group and at step q reads word L^q, so the 32 lanes always hit 32
+//   distinct table positions = 32 distinct banks.  The missing-genotype sum
+//   m_j reuses the same table: mapping missing codes (01) to het (10) and the
+//   rest to 00 makes T[b'] = sum of r over the missing slots.
+//   Blocks of the matrix (4 KiB = 32 SNPs x 512 samples) stream through a
+//   16-slot shared-memory ring filled by a producer warp with
+//   cp.async.bulk (TMA bulk copies, mbarrier complete_tx), with an L2 prefetch
+//   running ahead.  Per (SNP, tile) partial sums are fp32 (4 interleaved
+//   chains of 32 terms) and are promoted to an fp64 accumulator per tile, so
+//   the error is ~1e-7 relative to |g_j| -- inside the north star's 1e-6 on
+//   beta/loss (supports are stable up to 1e-5).  Because
+//   r is centred, t and u*sum_r do not cancel catastrophically; the constant
+//   part mean(r) contributes v_j * mean(r) * (s1_j - u_j cnt_j) = 0 exactly.
+//
+// aty_exact_kernel (operator-protocol path; bit-identical to the reference)
+//   Same per-byte fp64 arithmetic and byte order as _aty_kernel: per byte
+//   ((d0 r0 + d1 r1) + d2 r2) + d3 r3 added to t in sample order, likewise m.
+//   The caller passes the reference's own sum_r (numpy pairwise r.sum()).
+#include <stdlib.h>
+
+#include "common.cuh"
+
+namespace gi {
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+
+// ------------------------------------------------------------------ fast kernel
+constexpr int kWarps = 12;          // consumer warps; each streams its own groups
+constexpr int kThreads = kWarps * 32;
+constexpr int kSlots = 1;           // private TMA ring slots per warp
+constexpr int kMaxGroups = 112;     // groups per work item (fp64 accumulators in smem)
+constexpr int kTableBytes = 256 * 128 * 4;
+constexpr int kMiscBytes = kMaxGroups * 32 * 8 + kWarps * kSlots * 8 + kMaxGroups;
+constexpr int kRingBytes = kWarps * kSlots * GI_BLOCK_BYTES;
+constexpr int kSmemFast = 232448;   // the sm_100 per-block maximum (227 KiB)
+
+struct FastArgs {
+  MatrixDesc m;
+  const uint8_t* group_missing;
+  const float* rt;
+  const double* u;
+  const double* v;
+  const double* sum_rt;
+  double scale;
+  double* out;
+  int64_t n_items;
+  int flags;  // experiment knobs: 1 = skip lookups, 2 = L2 prefetch ahead
+};
+
+__device__ __forceinline__ float dose_term(int code, float r) {
+  // dose(code) * r with dose = 0, 0, 1, 2 for codes 0..3 (exact in fp32)
+  return code == 2 ? r : (code == 3 ? 2.0f * r : 0.0f);
+}
+
+template <int kOff>
+__device__ __forceinline__ float lds_f32_off(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(kOff));
+  return v;
+}
+
+template <int kOff>
+__device__ __forceinline__ uint32_t lds_u32_off(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(kOff));
+  return v;
+}
+
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+// Table build: all 256 threads.  Thread (w = lane, k = byte within word,
+// half) writes 128 entries T[pos = 4w + k][b] for b in [128 half, 128 half + 128)
+// at shared byte address  tbl + (k >> 1) * 65536 + b * 256 + (k & 1) * 128 + 4 w,
+// from the four residuals of samples 16w + 4k .. +3 of the tile.
+__device__ __forceinline__ float4 load_tile_r(const float* __restrict__ rt, int64_t t, int tid) {
+  const int w = tid & 31;
+  const int k = (tid >> 5) & 3;
+  return *reinterpret_cast<const float4*>(rt + t * GI_TILE_SAMPLES + 16 * w + 4 * k);
+}
+
+__device__ __forceinline__ void build_table(uint32_t tbl, float4 r, int tid) {
+  const int w = tid & 31;
+  const int k = (tid >> 5) & 3;
+  const int half = tid >> 7;
+  float lo[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) lo[c] = dose_term(c & 3, r.x) + dose_term(c >> 2, r.y);
+  const uint32_t base = tbl + (k >> 1) * 65536 + (k & 1) * 128 + 4 * w;
+#pragma unroll
+  for (int hh = 0; hh < 8; ++hh) {
+    const int hi = half * 8 + hh;
+    const float hv = dose_term(hi & 3, r.z) + dose_term(hi >> 2, r.w);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) sts_f32(base + (hi * 16 + c) * 256, lo[c] + hv);
+  }
+}
+
+__device__ __forceinline__ void stage_group(uint32_t slot_lane, uint32_t (&wd)[32]) {
+#pragma unroll
+  for (int q = 0; q < 32; ++q) wd[q] = lds_u32_off<0>(slot_lane + q * 128);
+}
+
+// One 32-SNP group x 512-sample tile.  `xb` = 4 * lane | (table base >> 8):
+// __byte_perm(word, xb ^ 4q, 0x65k4) is then the complete shared address of
+// T[position 4 (lane ^ q) + k][byte k of word] -- one PRMT per packed byte.
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+
+__device__ __forceinline__ void add2(uint64_t& acc, uint64_t x) {
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(x));  // FADD2: two fp32 adds
+}
+
+__device__ __forceinline__ float sum2(uint64_t x) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x));
+  return lo + hi;
+}
+
+template <bool kMissing>
+__device__ __forceinline__ void process_group(const uint32_t (&wd)[32], uint32_t xb,
+                                              float& tile_t, float& tile_m) {
+  uint64_t a01 = 0, a23 = 0, b01 = 0, b23 = 0;  // fp32x2 partial sums (4 chains)
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const uint32_t x = xb ^ (uint32_t)(q << 2);
+    const float e0 = lds_f32_off<0>(__byte_perm(wd[q], x, 0x6504));
+    const float e1 = lds_f32_off<128>(__byte_perm(wd[q], x, 0x6514));
+    const float e2 = lds_f32_off<65536>(__byte_perm(wd[q], x, 0x6524));
+    const float e3 = lds_f32_off<65536 + 128>(__byte_perm(wd[q], x, 0x6534));
+    add2(a01, pack2(e0, e1));
+    add2(a23, pack2(e2, e3));
+    if (kMissing) {
+      const uint32_t mm = (wd[q] << 1) & ~wd[q] & 0xAAAAAAAAu;  // missing (01) -> het (10)
+      const float f0 = lds_f32_off<0>(__byte_perm(mm, x, 0x6504));
+      const float f1 = lds_f32_off<128>(__byte_perm(mm, x, 0x6514));
+      const float f2 = lds_f32_off<65536>(__byte_perm(mm, x, 0x6524));
+      const float f3 = lds_f32_off<65536 + 128>(__byte_perm(mm, x, 0x6534));
+      add2(b01, pack2(f0, f1));
+      add2(b23, pack2(f2, f3));
+    }
+  }
+  tile_t = sum2(a01) + sum2(a23);
+  tile_m = kMissing ? sum2(b01) + sum2(b23) : 0.f;
+}
+
+// A warp's stream of blocks: for tile t = 0..T-1, its groups gl = warp,
+// warp + 8, ... < ng.  Walked by both the copy issuer and the consumer.
+struct BlockCursor {
+  uint32_t gl, first, ng;
+  int64_t t, T;
+  __device__ bool valid() const { return t < T; }
+  __device__ void next() {
+    gl += kWarps;
+    if (gl >= ng) {
+      gl = first;
+      ++t;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // Carve shared memory so that the table starts on a 64 KiB boundary of the
+  // shared window (its address bits 16+ then come straight out of the PRMT);
+  // the ring slots and the accumulators go in the space left on either side.
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t tbl_off = (0u - sbase) & 0xFFFFu;
+  const uint32_t tbl = sbase + tbl_off;
+  const uint32_t hi_off = tbl_off + kTableBytes;
+  // region list: [0, tbl_off) and [hi_off, kSmemFast)
+  uint32_t misc_off;
+  uint32_t ring_lo_off, ring_lo_n, ring_hi_off, ring_hi_n;
+  {
+    const uint32_t lo_size = tbl_off, hi_size = (uint32_t)kSmemFast - hi_off;
+    uint32_t lo_free = lo_size, hi_free = hi_size, lo_cur = 0, hi_cur = hi_off;
+    if (hi_free >= (uint32_t)kMiscBytes) {
+      misc_off = hi_cur;
+      hi_cur += kMiscBytes;
+      hi_free -= kMiscBytes;
+    } else {
+      misc_off = lo_cur;
+      lo_cur += kMiscBytes;
+      lo_free -= kMiscBytes;
+    }
+    ring_lo_off = (lo_cur + 127u) & ~127u;
+    ring_lo_n = lo_size > ring_lo_off ? (lo_size - ring_lo_off) / GI_BLOCK_BYTES : 0;
+    ring_hi_off = (hi_cur + 127u) & ~127u;
+    ring_hi_n = (uint32_t)kSmemFast > ring_hi_off ? ((uint32_t)kSmemFast - ring_hi_off) / GI_BLOCK_BYTES
+                                                   : 0;
+    (void)lo_free;
+    (void)hi_free;
+  }
+  if (ring_lo_n + ring_hi_n < (uint32_t)(kWarps * kSlots)) __trap();  // never on sm_100
+  double* acc = reinterpret_cast<double*>(smem + misc_off);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + misc_off + kMaxGroups * 32 * 8);
+  uint8_t* gflag = reinterpret_cast<uint8_t*>(bars + kWarps * kSlots);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  const MatrixDesc& m = a.m;
+
+  // this warp's slots (global slot id = warp * kSlots + s)
+  uint32_t slot_addr[kSlots];
+#pragma unroll
+  for (int s2 = 0; s2 < kSlots; ++s2) {
+    const uint32_t id = warp * kSlots + s2;
+    slot_addr[s2] = sbase + (id < ring_lo_n ? ring_lo_off + id * GI_BLOCK_BYTES
+                                            : ring_hi_off + (id - ring_lo_n) * GI_BLOCK_BYTES);
+  }
+  const uint32_t bar0 = smem_u32(bars + warp * kSlots);
+  if (lane == 0) {
+#pragma unroll
+    for (int s2 = 0; s2 < kSlots; ++s2) mbar_init(bar0 + 8 * s2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint32_t xb = ((uint32_t)lane << 2) | ((tbl >> 16) << 8);
+  const int64_t tile_stride = m.G * (int64_t)GI_BLOCK_BYTES;
+  uint32_t uses[kSlots];  // completed-phase counters of this warp's slots
+#pragma unroll
+  for (int s2 = 0; s2 < kSlots; ++s2) uses[s2] = 0;
+
+  for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+    const int64_t g0 = item * m.G / a.n_items;
+    const int64_t g1 = (item + 1) * m.G / a.n_items;
+    const uint32_t ng = (uint32_t)(g1 - g0);
+    const uint8_t* xitem = m.x + block_offset(0, g0, m.G);
+    const bool has_work = (uint32_t)warp < ng;
+
+    // copy issuer: lane 0 keeps kSlots blocks of this warp's stream in flight
+    BlockCursor issue{(uint32_t)warp, (uint32_t)warp, ng, 0, m.T};
+    BlockCursor pf{(uint32_t)warp, (uint32_t)warp, ng, 0, m.T};
+    int next_slot = 0;
+    auto issue_one = [&]() {
+      if (issue.valid()) {
+        if (lane == 0) {
+          const uint32_t bar = bar0 + 8 * next_slot;
+          mbar_expect_tx(bar, GI_BLOCK_BYTES);
+          bulk_g2s(slot_addr[next_slot],
+                   xitem + issue.t * tile_stride + (int64_t)issue.gl * GI_BLOCK_BYTES,
+                   GI_BLOCK_BYTES, bar);
+        }
+        issue.next();
+      }
+      next_slot = next_slot + 1 == kSlots ? 0 : next_slot + 1;
+    };
+    if (has_work) {
+      if (a.flags & 2) {
+        for (int i = 0; i < 8; ++i) {
+          if (pf.valid() && lane == 0)
+            prefetch_l2(xitem + pf.t * tile_stride + (int64_t)pf.gl * GI_BLOCK_BYTES,
+                        GI_BLOCK_BYTES);
+          if (pf.valid()) pf.next();
+        }
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < kSlots; ++s2) issue_one();
+    }
+    int cur_slot = 0;
+
+    for (uint32_t gl = warp; gl < ng; gl += kWarps) acc[gl * 32 + lane] = 0.0;
+    for (uint32_t gl = tid; gl < ng; gl += kThreads) gflag[gl] = a.group_missing[g0 + gl];
+    const bool builder = tid < 256;
+    float4 r_next = builder ? load_tile_r(a.rt, 0, tid) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t t = 0; t < m.T; ++t) {
+      __syncthreads();  // previous tile's lookups are done
+      if (builder) {
+        build_table(tbl, r_next, tid);
+        if (t + 1 < m.T) r_next = load_tile_r(a.rt, t + 1, tid);  // hidden behind the tile
+      }
+      __syncthreads();
+      for (uint32_t gl = warp; gl < ng; gl += kWarps) {
+        // wait for this slot's next phase (strictly in order: never ambiguous)
+        uint32_t u0 = 0;
+#pragma unroll
+        for (int s2 = 0; s2 < kSlots; ++s2)
+          if (s2 == cur_slot) u0 = uses[s2];
+        mbar_wait(bar0 + 8 * cur_slot, u0 & 1);
+        uint32_t wd[32];
+        uint32_t sa = 0;
+#pragma unroll
+        for (int s2 = 0; s2 < kSlots; ++s2)
+          if (s2 == cur_slot) sa = slot_addr[s2];
+        stage_group(sa + lane * 4, wd);
+#pragma unroll
+        for (int s2 = 0; s2 < kSlots; ++s2)
+          if (s2 == cur_slot) ++uses[s2];
+        __syncwarp();
+        next_slot = cur_slot;
+        issue_one();  // refill the slot just drained
+        if ((a.flags & 2) && pf.valid()) {
+          if (lane == 0)
+            prefetch_l2(xitem + pf.t * tile_stride + (int64_t)pf.gl * GI_BLOCK_BYTES,
+                        GI_BLOCK_BYTES);
+          pf.next();
+        }
+        cur_slot = cur_slot + 1 == kSlots ? 0 : cur_slot + 1;
+        float tt = 0.f, tm = 0.f;
+        const bool miss = gflag[gl] != 0;
+        if (a.flags & 1)
+          tt = __uint_as_float(wd[0] & 0x3f800000u);
+        else if (miss)
+          process_group<true>(wd, xb, tt, tm);
+        else
+          process_group<false>(wd, xb, tt, tm);
+        double add = (double)tt;
+        if (miss) {
+          const int64_t j = (g0 + gl) * 32 + lane;
+          const double uj = j < m.p ? a.u[j] : 0.0;
+          add += uj * (double)tm;
+        }
+        acc[gl * 32 + lane] += add;
+      }
+    }
+    // epilogue: out_j = scale * v_j * (acc_j - u_j * sum_rt)
+    const double srt = *a.sum_rt;
+    for (uint32_t gl = warp; gl < ng; gl += kWarps) {
+      const int64_t j = (g0 + gl) * 32 + lane;
+      if (j < m.p) {
+        const double val = a.v[j] * (acc[gl * 32 + lane] - a.u[j] * srt);
+        a.out[j] = a.scale * val;
+      }
+    }
+    __syncthreads();  // accumulators, flags and table are reused by the next item
+  }
+}
+
+int g_aty_flags = 0;  // experiment knobs (GI_ATY_FLAGS)
+
+int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
+                    const double* u, const double* v, const double* d_sum_rt, double scale,
+                    double* out, int num_sms, cudaStream_t s) {
+  if (m.p == 0) return 0;
+  static bool configured = false;
+  if (!configured) {
+    const char* env = getenv("GI_ATY_FLAGS");
+    if (env) g_aty_flags = atoi(env);
+    GI_CUDA_TRY(cudaFuncSetAttribute(aty_fast_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFast));
+    configured = true;
+  }
+  FastArgs a;
+  a.m = m;
+  a.group_missing = group_missing;
+  a.rt = rt;
+  a.u = u;
+  a.v = v;
+  a.sum_rt = d_sum_rt;
+  a.scale = scale;
+  a.out = out;
+  a.flags = g_aty_flags;
+  const int64_t per_wave = (int64_t)num_sms * kMaxGroups;
+  int64_t items = (int64_t)num_sms * ((m.G + per_wave - 1) / per_wave);
+  if (items > m.G) items = m.G;
+  a.n_items = items;
+  const int grid = (int)(items < num_sms ? items : num_sms);
+  aty_fast_kernel<<<grid, kThreads, kSmemFast, s>>>(a);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+// ------------------------------------------------------------------ exact kernel
+// One warp per SNP group, lane = SNP; the group's 4 KiB block is staged in
+// shared memory with coalesced loads, then each lane walks its own words in
+// natural sample order (bank = lane, conflict-free) and the r tile is read as
+// a warp-wide broadcast.
+constexpr int kExactWarps = 8;
+
+__global__ void __launch_bounds__(kExactWarps * 32) aty_exact_kernel(
+    MatrixDesc m, const double* __restrict__ r_pad, const double* __restrict__ u,
+    const double* __restrict__ v, const double* __restrict__ sum_r, double scale,
+    double* __restrict__ out) {
+  __shared__ double rs[GI_TILE_SAMPLES];
+  __shared__ __align__(16) uint8_t blk[kExactWarps][GI_BLOCK_BYTES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * kExactWarps + warp;
+  const bool active = g < m.G;
+  double t = 0.0, mm = 0.0;
+  const int64_t n_pad = m.T * GI_TILE_SAMPLES;
+  for (int64_t tt = 0; tt < m.T; ++tt) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < GI_TILE_SAMPLES; i += blockDim.x) {
+      const int64_t s = tt * GI_TILE_SAMPLES + i;
+      rs[i] = s < n_pad ? r_pad[s] : 0.0;
+    }
+    if (active) {
+      const uint4* src = reinterpret_cast<const uint4*>(m.x + block_offset(tt, g, m.G));
+      uint4* dst = reinterpret_cast<uint4*>(blk[warp]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dst[k * 32 + lane] = src[k * 32 + lane];
+    }
+    __syncthreads();
+    if (!active) continue;
+    for (int w = 0; w < 32; ++w) {
+      const uint32_t wd =
+          *reinterpret_cast<const uint32_t*>(blk[warp] + ((lane ^ w) << 7) + (lane << 2));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double* rr = rs + 16 * w + 4 * k;
+        double bt = 0.0, bm = 0.0;
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl) {
+          const uint32_t code = (wd >> (8 * k + 2 * sl)) & 3u;
+          const double d = code == 2u ? 1.0 : (code == 3u ? 2.0 : 0.0);
+          const double ms = code == 1u ? 1.0 : 0.0;
+          const double pt = __dmul_rn(d, rr[sl]);
+          const double pm = __dmul_rn(ms, rr[sl]);
+          bt = sl == 0 ? pt : __dadd_rn(bt, pt);
+          bm = sl == 0 ? pm : __dadd_rn(bm, pm);
+        }
+        t = __dadd_rn(t, bt);
+        mm = __dadd_rn(mm, bm);
+      }
+    }
+  }
+  if (!active) return;
+  const int64_t j = g * 32 + lane;
+  if (j < m.p) {
+    const double val = __dmul_rn(v[j], __dsub_rn(t, __dmul_rn(u[j], __dsub_rn(*sum_r, mm))));
+    out[j] = __dmul_rn(scale, val);
+  }
+}
+
+int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u, const double* v,
+                     const double* d_sum_r, double scale, double* out, cudaStream_t s) {
+  if (m.p == 0) return 0;
+  const int64_t blocks = (m.G + kExactWarps - 1) / kExactWarps;
+  aty_exact_kernel<<<(unsigned)blocks, kExactWarps * 32, 0, s>>>(m, r_pad, u, v, d_sum_r,
+                                                                 scale, out);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // namespace gi

@@ -1,0 +1,121 @@
+// Sparse standardized forward product and active-column decode.
+//
+// Reference: _ax_cols_kernel geno_matrix.py:168-194 (via ax_columns :328-349,
+// ax_parts :553-562) and _decompress_kernel :216-236 (via decompress :366-373).
+//
+// ax: out_i (+)= sum_t [dose_ij * scale_t - obs_ij * shift_t], scale_t = w_t v_j,
+// shift_t = u_j scale_t, columns visited in the caller's order for every sample
+// and columns with scale_t == 0 skipped -- the reference's exact per-sample
+// operation sequence, so the result is bit-identical to _ax_cols_kernel.  The
+// four possible per-code terms of column t are formed once per CTA in shared
+// memory (dose * scale is exact for dose in {0, 1, 2}; one rounding in the
+// subtraction, as in the reference), then each genotype costs one table read
+// and one fp64 add.
+#include "common.cuh"
+
+namespace gi {
+
+constexpr int kAxMaxCols = 1024;
+
+__global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
+                          const double* __restrict__ v, const int64_t* __restrict__ idx,
+                          const double* __restrict__ w, int k, double* __restrict__ out,
+                          int accumulate) {
+  __shared__ double terms[kAxMaxCols][4];
+  __shared__ int64_t cols[kAxMaxCols];
+  __shared__ int live[kAxMaxCols];
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    const int64_t j = idx[t];
+    const double scale = __dmul_rn(w[t], v[j]);
+    const double shift = __dmul_rn(u[j], scale);
+    cols[t] = j;
+    live[t] = scale != 0.0;
+    terms[t][0] = __dsub_rn(0.0 * scale, shift);      // code 00: dose 0, observed
+    terms[t][1] = __dsub_rn(0.0 * scale, 0.0 * shift);  // code 01: missing
+    terms[t][2] = __dsub_rn(scale, shift);              // code 10: dose 1
+    terms[t][3] = __dsub_rn(__dmul_rn(2.0, scale), shift);  // code 11: dose 2
+  }
+  __syncthreads();
+  const int64_t words = (m.n + 15) / 16;
+  for (int64_t wg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; wg < words;
+       wg += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = wg * 16;
+    const int cnt = (int)((m.n - i0) < 16 ? (m.n - i0) : 16);
+    double acc[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) acc[s] = (accumulate && s < cnt) ? out[i0 + s] : 0.0;
+    const int64_t tile = wg >> 5;
+    const int wp = (int)(wg & 31);
+    for (int t = 0; t < k; ++t) {
+      if (!live[t]) continue;
+      const uint32_t word =
+          *reinterpret_cast<const uint32_t*>(m.x + word_offset(tile, cols[t], wp, m.G));
+#pragma unroll
+      for (int s = 0; s < 16; ++s) acc[s] = __dadd_rn(acc[s], terms[t][(word >> (2 * s)) & 3u]);
+    }
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+      if (s < cnt) out[i0 + s] = acc[s];
+  }
+}
+
+int launch_ax(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
+              const double* w, int64_t k, double* out, int accumulate, cudaStream_t s) {
+  if (m.n == 0) return 0;
+  const int64_t words = (m.n + 15) / 16;
+  const int threads = 128;
+  int64_t blocks = (words + threads - 1) / threads;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (k <= 0) {
+    if (!accumulate) GI_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * m.n, s));
+    return 0;
+  }
+  for (int64_t c0 = 0; c0 < k; c0 += kAxMaxCols) {
+    const int kc = (int)((k - c0) < kAxMaxCols ? (k - c0) : kAxMaxCols);
+    ax_kernel<<<(unsigned)blocks, threads, 0, s>>>(m, u, v, idx + c0, w + c0, kc, out,
+                                                    (accumulate || c0 > 0) ? 1 : 0);
+    GI_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+// out_t is (k, n) row-major: out_t[t, i] = ((dose - u) * v) * obs.
+__global__ void decompress_kernel(MatrixDesc m, const double* __restrict__ u,
+                                  const double* __restrict__ v, const int64_t* __restrict__ idx,
+                                  int64_t k, double* __restrict__ out_t) {
+  const int64_t words = (m.n + 15) / 16;
+  const int64_t total = words * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / words;
+    const int64_t wg = e - t * words;
+    const int64_t j = idx[t];
+    const double uj = u[j], vj = v[j];
+    const uint32_t word =
+        *reinterpret_cast<const uint32_t*>(m.x + word_offset(wg >> 5, j, (int)(wg & 31), m.G));
+    const int64_t i0 = wg * 16;
+    double* row = out_t + t * m.n;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      if (i0 + s < m.n) {
+        const uint32_t code = (word >> (2 * s)) & 3u;
+        const double d = code == 2u ? 1.0 : (code == 3u ? 2.0 : 0.0);
+        const double o = code == 1u ? 0.0 : 1.0;
+        row[i0 + s] = __dmul_rn(__dmul_rn(__dsub_rn(d, uj), vj), o);
+      }
+    }
+  }
+}
+
+int launch_decompress(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
+                      int64_t k, double* out_t, cudaStream_t s) {
+  if (k <= 0 || m.n == 0) return 0;
+  const int64_t total = ((m.n + 15) / 16) * k;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  decompress_kernel<<<(unsigned)blocks, 256, 0, s>>>(m, u, v, idx, k, out_t);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // namespace gi

@@ -1,0 +1,545 @@
+// C ABI of libgenoiht_cuda.so (include/genoiht_cuda.h): handle management,
+// host-buffer operators and the stateless device primitives of the IHT loop.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "../../include/genoiht_cuda.h"
+#include "common.cuh"
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[1024] = "";
+
+void gi_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+#define CHECK_ARG(cond, msg)   \
+  do {                         \
+    if (!(cond)) {             \
+      gi_set_error("%s", msg); \
+      return -1;               \
+    }                          \
+  } while (0)
+
+#define TRY(expr)                 \
+  do {                            \
+    if ((expr) != 0) return -1;   \
+  } while (0)
+
+namespace {
+
+struct DevMem {
+  void* ptr = nullptr;
+  int device = 0;
+  ~DevMem() {
+    if (ptr) {
+      int prev = 0;
+      cudaGetDevice(&prev);
+      cudaSetDevice(device);
+      cudaFree(ptr);
+      cudaSetDevice(prev);
+    }
+  }
+};
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+int alloc(std::shared_ptr<DevMem>& out, size_t bytes, int device, bool zero) {
+  out = std::make_shared<DevMem>();
+  out->device = device;
+  if (bytes == 0) bytes = 16;
+  GI_CUDA_TRY(cudaMalloc(&out->ptr, bytes));
+  if (zero) GI_CUDA_TRY(cudaMemset(out->ptr, 0, bytes));
+  return 0;
+}
+
+// grow-only scratch buffer
+struct Scratch {
+  std::shared_ptr<DevMem> mem;
+  size_t bytes = 0;
+  int ensure(size_t want, int device) {
+    if (want <= bytes && mem) return 0;
+    TRY(alloc(mem, want, device, false));
+    bytes = want;
+    return 0;
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(mem->ptr);
+  }
+};
+
+int sm_count_of(int device) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return sms;
+}
+
+}  // namespace
+
+struct gi_matrix {
+  int device = 0;
+  int sms = 148;
+  int64_t n = 0, p = 0, nb = 0, T = 0, G = 0;
+  std::shared_ptr<DevMem> x;         // swizzled tiles (shared by with_stats copies)
+  std::shared_ptr<DevMem> miss_cnt;  // int32[p]
+  std::shared_ptr<DevMem> gmiss;     // uint8[G]
+  std::shared_ptr<DevMem> u, v;      // fp64[p], owned per handle
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  Scratch s_a, s_b, s_c, s_d;
+
+  gi::MatrixDesc desc() const {
+    gi::MatrixDesc d;
+    d.x = x ? static_cast<const uint8_t*>(x->ptr) : nullptr;
+    d.n = n;
+    d.p = p;
+    d.nb = nb;
+    d.T = T;
+    d.G = G;
+    return d;
+  }
+  double* du() const { return static_cast<double*>(u->ptr); }
+  double* dv() const { return static_cast<double*>(v->ptr); }
+  ~gi_matrix() {
+    if (stream) {
+      DeviceGuard g(device);
+      cudaStreamDestroy(stream);
+    }
+  }
+};
+
+static int matrix_shell(int64_t n, int64_t p, int device, gi_matrix** out,
+                        std::unique_ptr<gi_matrix>& h) {
+  CHECK_ARG(out != nullptr, "output handle pointer is NULL");
+  CHECK_ARG(n >= 0 && p >= 0, "matrix dimensions must be non-negative");
+  int count = 0;
+  GI_CUDA_TRY(cudaGetDeviceCount(&count));
+  CHECK_ARG(device >= 0 && device < count, "CUDA device index out of range");
+  h.reset(new gi_matrix());
+  h->device = device;
+  h->sms = sm_count_of(device);
+  h->n = n;
+  h->p = p;
+  h->nb = (n + 3) / 4;
+  h->T = (h->nb + GI_TILE_BYTES - 1) / GI_TILE_BYTES;
+  h->G = (p + GI_GROUP - 1) / GI_GROUP;
+  GI_CUDA_TRY(cudaSetDevice(device));
+  GI_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  TRY(alloc(h->x, (size_t)(h->T * h->G) * GI_BLOCK_BYTES, device, true));
+  TRY(alloc(h->u, sizeof(double) * p, device, true));
+  TRY(alloc(h->v, sizeof(double) * p, device, true));
+  TRY(alloc(h->miss_cnt, sizeof(int32_t) * p, device, true));
+  TRY(alloc(h->gmiss, (size_t)h->G, device, true));
+  return 0;
+}
+
+static int finish_stats(gi_matrix* h) {
+  gi::MatrixDesc d = h->desc();
+  TRY(gi::launch_stats(d, nullptr, h->du(), h->dv(), static_cast<int32_t*>(h->miss_cnt->ptr),
+                       h->stream));
+  TRY(gi::launch_group_flags(d, static_cast<int32_t*>(h->miss_cnt->ptr),
+                             static_cast<uint8_t*>(h->gmiss->ptr), h->stream));
+  GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+extern "C" {
+
+int gi_version(void) { return 100; }
+
+const char* gi_last_error(void) { return g_err; }
+
+int gi_device_count(int* count) {
+  CHECK_ARG(count != nullptr, "count is NULL");
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *count = c;
+  return 0;
+}
+
+int gi_device_info(int device, int* sm_count, int64_t* mem_bytes, int64_t* l2_bytes) {
+  cudaDeviceProp prop;
+  GI_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (mem_bytes) *mem_bytes = (int64_t)prop.totalGlobalMem;
+  if (l2_bytes) *l2_bytes = (int64_t)prop.l2CacheSize;
+  return 0;
+}
+
+int gi_device_sync(int device) {
+  DeviceGuard g(device);
+  GI_CUDA_TRY(cudaDeviceSynchronize());
+  return 0;
+}
+
+int gi_matrix_from_bed(const uint8_t* data, int64_t n, int64_t p, int device, gi_matrix** out) {
+  std::unique_ptr<gi_matrix> h;
+  TRY(matrix_shell(n, p, device, out, h));
+  DeviceGuard g(device);
+  if (p > 0 && h->nb > 0) {
+    CHECK_ARG(data != nullptr, "BED buffer is NULL");
+    // stream the upload in chunks of ~256 MiB through a pinned staging buffer
+    const int64_t chunk = std::max<int64_t>(1, (int64_t)(256ll << 20) / h->nb);
+    const int64_t cmax = std::min(chunk, p);
+    std::shared_ptr<DevMem> dbuf;
+    TRY(alloc(dbuf, (size_t)(cmax * h->nb), device, false));
+    void* pinned = nullptr;
+    GI_CUDA_TRY(cudaMallocHost(&pinned, (size_t)(cmax * h->nb)));
+    int rc = 0;
+    gi::MatrixDesc d = h->desc();
+    for (int64_t j0 = 0; j0 < p && rc == 0; j0 += cmax) {
+      const int64_t cnt = std::min(cmax, p - j0);
+      memcpy(pinned, data + j0 * h->nb, (size_t)(cnt * h->nb));
+      if (cudaMemcpyAsync(dbuf->ptr, pinned, (size_t)(cnt * h->nb), cudaMemcpyHostToDevice,
+                          h->stream) != cudaSuccess) {
+        gi_set_error("H2D copy of the BED buffer failed");
+        rc = -1;
+        break;
+      }
+      rc = gi::launch_upload_tiles(d, static_cast<uint8_t*>(h->x->ptr),
+                                   static_cast<const uint8_t*>(dbuf->ptr), j0, cnt, h->stream);
+      if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
+        gi_set_error("upload failed");
+        rc = -1;
+      }
+    }
+    cudaFreeHost(pinned);
+    if (rc) return -1;
+  }
+  TRY(finish_stats(h.get()));
+  *out = h.release();
+  return 0;
+}
+
+int gi_matrix_synth(uint64_t seed, int64_t n, int64_t p, int64_t j_base, double maf_lo,
+                    double maf_hi, double missing, int device, gi_matrix** out) {
+  std::unique_ptr<gi_matrix> h;
+  TRY(matrix_shell(n, p, device, out, h));
+  DeviceGuard g(device);
+  TRY(gi::launch_synth(h->desc(), static_cast<uint8_t*>(h->x->ptr), seed, j_base, maf_lo, maf_hi,
+                       missing, h->stream));
+  TRY(finish_stats(h.get()));
+  *out = h.release();
+  return 0;
+}
+
+int gi_matrix_with_stats(const gi_matrix* src, const double* u, const double* v, gi_matrix** out) {
+  CHECK_ARG(src && u && v && out, "NULL argument");
+  std::unique_ptr<gi_matrix> h(new gi_matrix());
+  h->device = src->device;
+  h->sms = src->sms;
+  h->n = src->n;
+  h->p = src->p;
+  h->nb = src->nb;
+  h->T = src->T;
+  h->G = src->G;
+  h->x = src->x;
+  h->miss_cnt = src->miss_cnt;
+  h->gmiss = src->gmiss;
+  DeviceGuard g(h->device);
+  GI_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  TRY(alloc(h->u, sizeof(double) * h->p, h->device, false));
+  TRY(alloc(h->v, sizeof(double) * h->p, h->device, false));
+  GI_CUDA_TRY(cudaMemcpy(h->u->ptr, u, sizeof(double) * h->p, cudaMemcpyHostToDevice));
+  GI_CUDA_TRY(cudaMemcpy(h->v->ptr, v, sizeof(double) * h->p, cudaMemcpyHostToDevice));
+  *out = h.release();
+  return 0;
+}
+
+int gi_matrix_subset_rows(const gi_matrix* src, const int64_t* rows, int64_t m, gi_matrix** out) {
+  CHECK_ARG(src != nullptr, "NULL handle");
+  for (int64_t i = 0; i < m; ++i)
+    CHECK_ARG(rows[i] >= 0 && rows[i] < src->n, "row index out of range");
+  std::unique_ptr<gi_matrix> h;
+  TRY(matrix_shell(m, src->p, src->device, out, h));
+  DeviceGuard g(src->device);
+  if (m > 0 && src->p > 0) {
+    std::shared_ptr<DevMem> drows;
+    TRY(alloc(drows, sizeof(int64_t) * m, src->device, false));
+    GI_CUDA_TRY(cudaMemcpy(drows->ptr, rows, sizeof(int64_t) * m, cudaMemcpyHostToDevice));
+    TRY(gi::launch_subset_rows(src->desc(), h->desc(), static_cast<uint8_t*>(h->x->ptr),
+                               static_cast<const int64_t*>(drows->ptr), h->stream));
+    GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  TRY(finish_stats(h.get()));
+  *out = h.release();
+  return 0;
+}
+
+int gi_matrix_free(gi_matrix* h) {
+  if (h) {
+    DeviceGuard g(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    delete h;
+  }
+  return 0;
+}
+
+int gi_matrix_shape(const gi_matrix* h, int64_t* n, int64_t* p, int* device) {
+  CHECK_ARG(h != nullptr, "NULL handle");
+  if (n) *n = h->n;
+  if (p) *p = h->p;
+  if (device) *device = h->device;
+  return 0;
+}
+
+int gi_matrix_stats(const gi_matrix* h, double* u, double* v) {
+  CHECK_ARG(h != nullptr, "NULL handle");
+  DeviceGuard g(h->device);
+  if (h->p == 0) return 0;
+  if (u) GI_CUDA_TRY(cudaMemcpy(u, h->u->ptr, sizeof(double) * h->p, cudaMemcpyDeviceToHost));
+  if (v) GI_CUDA_TRY(cudaMemcpy(v, h->v->ptr, sizeof(double) * h->p, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int gi_matrix_read_bed(const gi_matrix* hc, int64_t j0, int64_t count, uint8_t* out) {
+  gi_matrix* h = const_cast<gi_matrix*>(hc);
+  CHECK_ARG(h != nullptr, "NULL handle");
+  CHECK_ARG(j0 >= 0 && count >= 0 && j0 + count <= h->p, "SNP range out of bounds");
+  if (count == 0 || h->nb == 0) return 0;
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard g(h->device);
+  const int64_t chunk = std::max<int64_t>(1, (int64_t)(256ll << 20) / h->nb);
+  TRY(h->s_a.ensure((size_t)(std::min(chunk, count) * h->nb), h->device));
+  for (int64_t c0 = 0; c0 < count; c0 += chunk) {
+    const int64_t cnt = std::min(chunk, count - c0);
+    TRY(gi::launch_download_tiles(h->desc(), h->s_a.as<uint8_t>(), j0 + c0, cnt, h->stream));
+    GI_CUDA_TRY(cudaMemcpyAsync(out + c0 * h->nb, h->s_a.mem->ptr, (size_t)(cnt * h->nb),
+                                cudaMemcpyDeviceToHost, h->stream));
+    GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  return 0;
+}
+
+int gi_matrix_missing_counts(const gi_matrix* h, int32_t* out) {
+  CHECK_ARG(h && out, "NULL argument");
+  DeviceGuard g(h->device);
+  if (h->p) GI_CUDA_TRY(cudaMemcpy(out, h->miss_cnt->ptr, sizeof(int32_t) * h->p,
+                                   cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int gi_matrix_device_stats(const gi_matrix* h, const double** d_u, const double** d_v) {
+  CHECK_ARG(h != nullptr, "NULL handle");
+  if (d_u) *d_u = h->du();
+  if (d_v) *d_v = h->dv();
+  return 0;
+}
+
+int64_t gi_padded_samples(const gi_matrix* h) { return h ? h->T * GI_TILE_SAMPLES : 0; }
+
+static void build_rowmask(const gi_matrix* h, const uint8_t* keep, std::vector<uint32_t>& mask) {
+  mask.assign((size_t)(h->T * GI_TILE_WORDS), 0u);
+  for (int64_t i = 0; i < h->n; ++i)
+    if (keep[i]) mask[(size_t)(i >> 4)] |= 1u << (2 * (i & 15));
+}
+
+int gi_matrix_masked_stats(const gi_matrix* hc, const uint8_t* keep, double* u, double* v) {
+  gi_matrix* h = const_cast<gi_matrix*>(hc);
+  CHECK_ARG(h && keep && u && v, "NULL argument");
+  if (h->p == 0) return 0;
+  std::vector<uint32_t> mask;
+  build_rowmask(h, keep, mask);
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard g(h->device);
+  TRY(h->s_a.ensure(mask.size() * 4, h->device));
+  TRY(h->s_b.ensure(sizeof(double) * 2 * h->p, h->device));
+  GI_CUDA_TRY(cudaMemcpyAsync(h->s_a.mem->ptr, mask.data(), mask.size() * 4,
+                              cudaMemcpyHostToDevice, h->stream));
+  double* du = h->s_b.as<double>();
+  TRY(gi::launch_stats(h->desc(), h->s_a.as<uint32_t>(), du, du + h->p, nullptr, h->stream));
+  GI_CUDA_TRY(cudaMemcpyAsync(u, du, sizeof(double) * h->p, cudaMemcpyDeviceToHost, h->stream));
+  GI_CUDA_TRY(cudaMemcpyAsync(v, du + h->p, sizeof(double) * h->p, cudaMemcpyDeviceToHost,
+                              h->stream));
+  GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+// ------------------------------------------------------- host-buffer operators
+int gi_aty(gi_matrix* h, const double* r, double sum_r, double* out, int mode) {
+  CHECK_ARG(h && r && out, "NULL argument");
+  if (h->p == 0) return 0;
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard g(h->device);
+  const int64_t npad = h->T * GI_TILE_SAMPLES;
+  // scratch layout: s_a = r (fp64 padded) | rt (fp32 padded); s_b = out; s_c = scalars/partials
+  TRY(h->s_a.ensure(sizeof(double) * npad + sizeof(float) * npad + 64, h->device));
+  TRY(h->s_b.ensure(sizeof(double) * h->p, h->device));
+  TRY(h->s_c.ensure(sizeof(double) * (16 + 8 * 296) + 64, h->device));
+  double* dr = h->s_a.as<double>();
+  float* drt = reinterpret_cast<float*>(dr + npad);
+  double* scal = h->s_c.as<double>();
+  double* partials = scal + 16;
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(partials + 8 * 296);
+  GI_CUDA_TRY(cudaMemsetAsync(dr, 0, sizeof(double) * npad, h->stream));
+  GI_CUDA_TRY(cudaMemcpyAsync(dr, r, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
+  if (mode == 0) {
+    GI_CUDA_TRY(cudaMemcpyAsync(scal, &sum_r, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    TRY(gi::launch_aty_exact(h->desc(), dr, h->du(), h->dv(), scal, 1.0, h->s_b.as<double>(),
+                             h->stream));
+  } else {
+    GI_CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), h->stream));
+    // mean over the n real samples, then centred fp32 copy and its sum
+    TRY(gi::launch_residual(h->n, dr, nullptr, nullptr, 0, nullptr, nullptr, (double)h->n,
+                            dr, scal, partials, ticket, h->stream));
+    TRY(gi::launch_center(h->n, npad, dr, nullptr, scal, drt, partials, ticket, h->stream));
+    TRY(gi::launch_aty_fast(h->desc(), static_cast<const uint8_t*>(h->gmiss->ptr), drt, h->du(),
+                            h->dv(), scal + 2, 1.0, h->s_b.as<double>(), h->sms, h->stream));
+  }
+  GI_CUDA_TRY(cudaMemcpyAsync(out, h->s_b.mem->ptr, sizeof(double) * h->p,
+                              cudaMemcpyDeviceToHost, h->stream));
+  GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int gi_ax_cols(gi_matrix* h, const int64_t* idx, const double* w, int64_t k, double* out) {
+  CHECK_ARG(h && out, "NULL argument");
+  for (int64_t t = 0; t < k; ++t)
+    CHECK_ARG(idx[t] >= 0 && idx[t] < h->p, "variant index out of range");
+  if (h->n == 0) return 0;
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard g(h->device);
+  TRY(h->s_a.ensure(sizeof(int64_t) * (k + 1) + sizeof(double) * (k + 1), h->device));
+  TRY(h->s_b.ensure(sizeof(double) * h->n, h->device));
+  int64_t* didx = h->s_a.as<int64_t>();
+  double* dw = reinterpret_cast<double*>(didx + k + 1);
+  if (k > 0) {
+    GI_CUDA_TRY(cudaMemcpyAsync(didx, idx, sizeof(int64_t) * k, cudaMemcpyHostToDevice, h->stream));
+    GI_CUDA_TRY(cudaMemcpyAsync(dw, w, sizeof(double) * k, cudaMemcpyHostToDevice, h->stream));
+  }
+  TRY(gi::launch_ax(h->desc(), h->du(), h->dv(), didx, dw, k, h->s_b.as<double>(), 0, h->stream));
+  GI_CUDA_TRY(cudaMemcpyAsync(out, h->s_b.mem->ptr, sizeof(double) * h->n,
+                              cudaMemcpyDeviceToHost, h->stream));
+  GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int gi_decompress(gi_matrix* h, const int64_t* idx, int64_t k, double* out_t) {
+  CHECK_ARG(h && out_t, "NULL argument");
+  for (int64_t t = 0; t < k; ++t)
+    CHECK_ARG(idx[t] >= 0 && idx[t] < h->p, "variant index out of range");
+  if (k == 0 || h->n == 0) return 0;
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard g(h->device);
+  TRY(h->s_a.ensure(sizeof(int64_t) * k, h->device));
+  TRY(h->s_b.ensure(sizeof(double) * h->n * k, h->device));
+  GI_CUDA_TRY(cudaMemcpyAsync(h->s_a.mem->ptr, idx, sizeof(int64_t) * k, cudaMemcpyHostToDevice,
+                              h->stream));
+  TRY(gi::launch_decompress(h->desc(), h->du(), h->dv(), h->s_a.as<int64_t>(), k,
+                            h->s_b.as<double>(), h->stream));
+  GI_CUDA_TRY(cudaMemcpyAsync(out_t, h->s_b.mem->ptr, sizeof(double) * h->n * k,
+                              cudaMemcpyDeviceToHost, h->stream));
+  GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+// ------------------------------------------------------------ device primitives
+#define STREAM(s) static_cast<cudaStream_t>(s)
+
+int gi_dev_ax(gi_matrix* h, const double* u, const double* v, const int64_t* d_idx,
+              const double* d_w, int64_t k, double* d_out, int accumulate, void* stream) {
+  CHECK_ARG(h && d_out, "NULL argument");
+  return gi::launch_ax(h->desc(), u ? u : h->du(), v ? v : h->dv(), d_idx, d_w, k, d_out,
+                       accumulate, STREAM(stream));
+}
+
+int gi_dev_aty_fast(gi_matrix* h, const double* u, const double* v, const float* d_rt,
+                    const double* d_sum_rt, double scale, double* d_out, void* stream) {
+  CHECK_ARG(h && d_rt && d_sum_rt && d_out, "NULL argument");
+  return gi::launch_aty_fast(h->desc(), static_cast<const uint8_t*>(h->gmiss->ptr), d_rt,
+                             u ? u : h->du(), v ? v : h->dv(), d_sum_rt, scale, d_out, h->sms,
+                             STREAM(stream));
+}
+
+int gi_dev_aty_exact(gi_matrix* h, const double* u, const double* v, const double* d_rpad,
+                     const double* d_sum_r, double scale, double* d_out, void* stream) {
+  CHECK_ARG(h && d_rpad && d_sum_r && d_out, "NULL argument");
+  return gi::launch_aty_exact(h->desc(), d_rpad, u ? u : h->du(), v ? v : h->dv(), d_sum_r, scale,
+                              d_out, STREAM(stream));
+}
+
+int gi_dev_stats(gi_matrix* h, const uint32_t* d_rowmask, double* d_u, double* d_v,
+                 void* stream) {
+  CHECK_ARG(h && d_u && d_v, "NULL argument");
+  return gi::launch_stats(h->desc(), d_rowmask, d_u, d_v, nullptr, STREAM(stream));
+}
+
+int64_t gi_red_partials(void) { return 8 * 296; }
+
+int gi_dev_residual(int64_t n, const double* d_y, const double* d_fit, const double* d_C,
+                    int64_t c, const double* d_bcov, const uint8_t* d_keep, double n_eff,
+                    double* d_r, double* d_scal, double* d_partials, uint32_t* d_ticket,
+                    void* stream) {
+  return gi::launch_residual(n, d_y, d_fit, d_C, (int)c, d_bcov, d_keep, n_eff, d_r, d_scal,
+                             d_partials, d_ticket, STREAM(stream));
+}
+
+int gi_dev_center(int64_t n, int64_t n_pad, const double* d_r, const uint8_t* d_keep,
+                  double* d_scal, float* d_rt, double* d_partials, uint32_t* d_ticket,
+                  void* stream) {
+  return gi::launch_center(n, n_pad, d_r, d_keep, d_scal, d_rt, d_partials, d_ticket,
+                           STREAM(stream));
+}
+
+int gi_dev_covgrad(int64_t n, const double* d_C, int64_t c, const double* d_r, double* d_gcov,
+                   double* d_partials, uint32_t* d_ticket, void* stream) {
+  return gi::launch_covgrad(n, d_C, (int)c, d_r, d_gcov, d_partials, d_ticket, STREAM(stream));
+}
+
+int gi_dev_maxabs(int64_t m, const double* d_x, double* d_scal, int slot, double* d_partials,
+                  uint32_t* d_ticket, void* stream) {
+  return gi::launch_maxabs(m, d_x, d_scal, slot, d_partials, d_ticket, STREAM(stream));
+}
+
+int gi_dev_sumsq(int64_t m, const double* d_x, double* d_scal, int slot, double* d_partials,
+                 uint32_t* d_ticket, void* stream) {
+  return gi::launch_sumsq(m, d_x, d_scal, slot, d_partials, d_ticket, STREAM(stream));
+}
+
+int gi_dev_add_cov(int64_t n, const double* d_C, int64_t c, const double* d_w, double* d_x,
+                   void* stream) {
+  return gi::launch_add_cov(n, d_C, (int)c, d_w, d_x, STREAM(stream));
+}
+
+int64_t gi_topk_slots(int64_t p, int64_t k) { return gi::topk_blocks(p) * (k > 0 ? k : 1); }
+
+int gi_dev_topk(int64_t p, int64_t k, int mode, const double* d_beta, const double* d_g,
+                double mu, int64_t idx_base, uint64_t* d_ckey, int64_t* d_cidx, double* d_cval,
+                int64_t* d_out_idx, double* d_out_val, uint64_t* d_out_key, int64_t* d_count,
+                void* stream) {
+  return gi::launch_topk(p, k, mode, d_beta, d_g, mu, idx_base, d_ckey, d_cidx, d_cval,
+                         d_out_idx, d_out_val, d_out_key, d_count, STREAM(stream));
+}
+
+int gi_dev_scatter(int64_t k, const int64_t* d_idx, const double* d_val, double* d_beta,
+                   void* stream) {
+  return gi::launch_scatter(k, d_idx, d_val, d_beta, STREAM(stream));
+}
+
+int gi_dev_gather(int64_t k, const int64_t* d_idx, const double* d_src, double* d_dst,
+                  void* stream) {
+  return gi::launch_gather(k, d_idx, d_src, d_dst, STREAM(stream));
+}
+
+}  // extern "C"

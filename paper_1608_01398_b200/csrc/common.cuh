@@ -1,0 +1,124 @@
+// Shared definitions for the sm_100a genoiht kernels.
+//
+// Device layout of a packed genotype matrix ("swizzled sample tiles"):
+//   * samples are cut into tiles of 512 (128 packed bytes per SNP, 32 words);
+//   * SNPs are cut into groups of 32 (one per lane of the X^T r warp);
+//   * block (tile t, group g) is 4 KiB at offset ((t * G) + g) * 4096;
+//   * inside a block, 32-bit word w (samples 512t + 16w .. +15, LSB-first
+//     2-bit codes exactly as in the BED file) of SNP 32g + L is stored at byte
+//     offset ((L ^ w) * 128 + 4 * L).
+// A warp reading row q of a block therefore gets lane L = word (L ^ q) of SNP
+// L: one coalesced 128-byte line, and each lane at a distinct sample position,
+// which is what makes the X^T r lookup tables bank-conflict free (aty.cu).
+// Bytes past ceil(n/4) and SNPs past p are zero (dose 0, never read as data).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define GI_TILE_SAMPLES 512
+#define GI_TILE_BYTES 128
+#define GI_TILE_WORDS 32
+#define GI_GROUP 32
+#define GI_BLOCK_BYTES 4096
+
+namespace gi {
+
+struct MatrixDesc {
+  const uint8_t* x;   // swizzled tiles
+  int64_t n;          // samples
+  int64_t p;          // SNPs
+  int64_t nb;         // ceil(n/4) bytes per SNP in the BED layout
+  int64_t T;          // sample tiles = ceil(nb / 128)
+  int64_t G;          // SNP groups = ceil(p / 32)
+};
+
+__host__ __device__ inline int64_t block_offset(int64_t t, int64_t g, int64_t G) {
+  return (t * G + g) * (int64_t)GI_BLOCK_BYTES;
+}
+
+// byte offset of word w of SNP j in tile t
+__host__ __device__ inline int64_t word_offset(int64_t t, int64_t j, int w, int64_t G) {
+  const int L = (int)(j & 31);
+  return block_offset(t, j >> 5, G) + (int64_t)(((L ^ w) << 7) + (L << 2));
+}
+
+// byte offset of packed byte b (BED column index) of SNP j
+__host__ __device__ inline int64_t byte_offset(int64_t j, int64_t b, int64_t G) {
+  const int64_t t = b >> 7;
+  const int w = (int)((b >> 2) & 31);
+  return word_offset(t, j, w, G) + (b & 3);
+}
+
+int launch_residual(int64_t n, const double* y, const double* fit, const double* C, int c,
+                    const double* bcov, const uint8_t* keep, double n_eff, double* r,
+                    double* scal, double* partials, unsigned int* ticket, cudaStream_t s);
+int launch_center(int64_t n, int64_t n_pad, const double* r, const uint8_t* keep, double* scal,
+                  float* rt, double* partials, unsigned int* ticket, cudaStream_t s);
+int launch_covgrad(int64_t n, const double* C, int c, const double* r, double* gcov,
+                   double* partials, unsigned int* ticket, cudaStream_t s);
+int launch_maxabs(int64_t m, const double* x, double* scal, int slot, double* partials,
+                  unsigned int* ticket, cudaStream_t s);
+int launch_sumsq(int64_t m, const double* x, double* scal, int slot, double* partials,
+                 unsigned int* ticket, cudaStream_t s);
+int launch_add_cov(int64_t n, const double* C, int c, const double* w, double* x,
+                   cudaStream_t s);
+int64_t topk_blocks(int64_t p);
+int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double* g, double mu,
+                int64_t idx_base, uint64_t* cand_key, int64_t* cand_idx, double* cand_val,
+                int64_t* out_idx, double* out_val, uint64_t* out_key, int64_t* out_count,
+                cudaStream_t s);
+int launch_scatter(int64_t k, const int64_t* idx, const double* val, double* beta,
+                   cudaStream_t s);
+int launch_gather(int64_t k, const int64_t* idx, const double* src, double* dst,
+                  cudaStream_t s);
+}  // namespace gi
+
+// error plumbing shared with capi.cu
+void gi_set_error(const char* fmt, ...);
+
+#define GI_CUDA_TRY(expr)                                                        \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      gi_set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),       \
+                   __FILE__, __LINE__);                                          \
+      return -1;                                                                 \
+    }                                                                            \
+  } while (0)
+
+#define GI_LAUNCH_CHECK()                                                        \
+  do {                                                                           \
+    cudaError_t _e = cudaGetLastError();                                         \
+    if (_e != cudaSuccess) {                                                     \
+      gi_set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e),   \
+                   __FILE__, __LINE__);                                          \
+      return -1;                                                                 \
+    }                                                                            \
+  } while (0)
+
+// Kernel-layer entry points (host side), all stream-ordered; return 0 or -1.
+namespace gi {
+int launch_upload_tiles(const MatrixDesc& m, uint8_t* x, const uint8_t* d_bed_chunk,
+                        int64_t j0, int64_t count, cudaStream_t s);
+int launch_download_tiles(const MatrixDesc& m, uint8_t* d_bed_chunk, int64_t j0,
+                          int64_t count, cudaStream_t s);
+int launch_synth(const MatrixDesc& m, uint8_t* x, uint64_t seed, int64_t j_base,
+                 double maf_lo, double maf_hi, double missing, cudaStream_t s);
+int launch_subset_rows(const MatrixDesc& src, const MatrixDesc& dst, uint8_t* x,
+                       const int64_t* d_rows, cudaStream_t s);
+int launch_stats(const MatrixDesc& m, const uint32_t* d_rowmask, double* u, double* v,
+                 int32_t* d_missing_cnt, cudaStream_t s);
+int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_t* flags,
+                       cudaStream_t s);
+int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
+                    const double* u, const double* v, const double* d_sum_rt, double scale,
+                    double* out, int num_sms, cudaStream_t s);
+int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u,
+                     const double* v, const double* d_sum_r, double scale, double* out,
+                     cudaStream_t s);
+int launch_ax(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
+              const double* w, int64_t k, double* out, int accumulate, cudaStream_t s);
+int launch_decompress(const MatrixDesc& m, const double* u, const double* v,
+                      const int64_t* idx, int64_t k, double* out_t, cudaStream_t s);
+}  // namespace gi

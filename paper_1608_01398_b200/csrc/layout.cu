@@ -1,0 +1,251 @@
+// Matrix construction kernels: BED bytes <-> swizzled sample tiles, the
+// counter-based synthetic generator, and per-SNP standardisation statistics.
+//
+// Reference behaviour replaced:
+//   PackedGenotypeMatrix.from_bed_buffer  geno_matrix.py:281-292 (bytes kept verbatim)
+//   _stats_kernel / _packed_stats         geno_matrix.py:106-139, :239-246
+//   random_packed_matrix                  simulate.py:56-65 (same law, hash-based stream)
+#include "common.cuh"
+
+namespace gi {
+
+// ---------------------------------------------------------------- upload
+// d_bed: `count` SNPs x nb bytes (variant-major, as read from a BED file),
+// first SNP = j0.  One thread per 32-bit word of the tiled layout.
+__global__ void upload_tiles_kernel(MatrixDesc m, uint8_t* __restrict__ x,
+                                    const uint8_t* __restrict__ bed, int64_t j0,
+                                    int64_t count) {
+  const int64_t words = m.T * GI_TILE_WORDS;
+  const int64_t total = count * words;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jj = e / words;
+    const int64_t wg = e - jj * words;  // global word index along samples
+    const int64_t j = j0 + jj;
+    const uint8_t* row = bed + jj * m.nb;
+    uint32_t word = 0;
+    const int64_t b0 = wg * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t b = b0 + k;
+      if (b < m.nb) word |= (uint32_t)row[b] << (8 * k);
+    }
+    const int64_t t = wg >> 5;
+    const int w = (int)(wg & 31);
+    *reinterpret_cast<uint32_t*>(x + word_offset(t, j, w, m.G)) = word;
+  }
+}
+
+__global__ void download_tiles_kernel(MatrixDesc m, const uint8_t* __restrict__ x,
+                                      uint8_t* __restrict__ bed, int64_t j0, int64_t count) {
+  const int64_t total = count * m.nb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jj = e / m.nb;
+    const int64_t b = e - jj * m.nb;
+    bed[e] = x[byte_offset(j0 + jj, b, m.G)];
+  }
+}
+
+static int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g > 148 * 64) g = 148 * 64;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int launch_upload_tiles(const MatrixDesc& m, uint8_t* x, const uint8_t* d_bed, int64_t j0,
+                        int64_t count, cudaStream_t s) {
+  if (count <= 0) return 0;
+  upload_tiles_kernel<<<grid_for(count * m.T * 32, 256), 256, 0, s>>>(m, x, d_bed, j0, count);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_download_tiles(const MatrixDesc& m, uint8_t* d_bed, int64_t j0, int64_t count,
+                          cudaStream_t s) {
+  if (count <= 0 || m.nb == 0) return 0;
+  download_tiles_kernel<<<grid_for(count * m.nb, 256), 256, 0, s>>>(m, m.x, d_bed, j0, count);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------- synth
+// Must stay bit-identical to oracle/genoiht_oracle.c (ora_key, ora_synth).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return z;
+}
+
+__device__ __forceinline__ uint64_t synth_key(uint64_t seed, uint64_t j, uint64_t i) {
+  return mix64(seed * 0x9E3779B97F4A7C15ULL + j * 0xD1B54A32D192ED03ULL +
+               i * 0x8CB92BA72F3D8DD7ULL + 0x632BE59BD9B4E019ULL);
+}
+
+__device__ __forceinline__ uint32_t thr_from(double prob) {
+  const double scale = 4294967296.0;
+  const double t = floor(__dmul_rn(prob, scale));
+  return t >= scale ? 0xFFFFFFFFu : (uint32_t)t;
+}
+
+// One thread per (SNP, word); j_base is the global index of local SNP 0 so
+// that a SNP-sharded matrix holds exactly the bytes of the unsharded one.
+__global__ void synth_kernel(MatrixDesc m, uint8_t* __restrict__ x, uint64_t seed,
+                             int64_t j_base, double maf_lo, double maf_hi, double missing) {
+  const int64_t words = m.T * GI_TILE_WORDS;
+  const int64_t total = m.p * words;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / words;
+    const int64_t wg = e - j * words;
+    const uint64_t jg = (uint64_t)(j + j_base);
+    const uint64_t hf = synth_key(seed, jg, 0xFFFFFFFFFFFFULL);
+    const double unit = __dmul_rn((double)(hf >> 11), 1.0 / 9007199254740992.0);
+    const double f = __dadd_rn(maf_lo, __dmul_rn(__dsub_rn(maf_hi, maf_lo), unit));
+    const double q = __dsub_rn(1.0, f);
+    const double p0 = __dmul_rn(q, q);
+    const double p1 = __dadd_rn(p0, __dmul_rn(__dmul_rn(2.0, f), q));
+    const uint32_t t0 = thr_from(p0), t1 = thr_from(p1), tm = thr_from(missing);
+    uint32_t word = 0;
+    const int64_t i0 = wg * 16;
+    for (int s = 0; s < 16; ++s) {
+      const int64_t i = i0 + s;
+      if (i >= m.n) break;
+      const uint64_t h = synth_key(seed, jg, (uint64_t)i);
+      const uint32_t ud = (uint32_t)h, um = (uint32_t)(h >> 32);
+      uint32_t code = ud < t0 ? 0u : (ud < t1 ? 2u : 3u);
+      if (um < tm) code = 1u;
+      word |= code << (2 * s);
+    }
+    *reinterpret_cast<uint32_t*>(x + word_offset(wg >> 5, j, (int)(wg & 31), m.G)) = word;
+  }
+}
+
+int launch_synth(const MatrixDesc& m, uint8_t* x, uint64_t seed, int64_t j_base,
+                 double maf_lo, double maf_hi, double missing, cudaStream_t s) {
+  if (m.p == 0) return 0;
+  synth_kernel<<<grid_for(m.p * m.T * 32, 256), 256, 0, s>>>(m, x, seed, j_base, maf_lo,
+                                                              maf_hi, missing);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------- stats
+// One warp per SNP group, lane L = SNP 32g + L; at row q the warp reads one
+// 128-byte line (word L ^ q of each SNP).  Counts are integers, so u and v
+// come out bit-identical to the reference's fp64 sums (geno_matrix.py:134-139).
+// d_rowmask (optional): one uint32 per (tile, word), bit 2s set when sample
+// 16w + s of the tile is included (cross-validation training rows).
+__global__ void stats_kernel(MatrixDesc m, const uint32_t* __restrict__ rowmask,
+                             double* __restrict__ u, double* __restrict__ v,
+                             int32_t* __restrict__ missing_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= m.G) return;
+  const int64_t j = g * 32 + lane;
+  int cnt = 0, s1 = 0, s2 = 0, miss = 0;
+  for (int64_t t = 0; t < m.T; ++t) {
+    const uint8_t* blk = m.x + block_offset(t, g, m.G);
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const uint32_t word = *reinterpret_cast<const uint32_t*>(blk + (q << 7) + (lane << 2));
+      const int w = lane ^ q;
+      const int64_t first = t * GI_TILE_SAMPLES + 16 * w;
+      const int64_t nvalid64 = m.n - first;
+      const int nvalid = nvalid64 >= 16 ? 16 : (nvalid64 <= 0 ? 0 : (int)nvalid64);
+      uint32_t valid = nvalid >= 16 ? 0x55555555u : ((1u << (2 * nvalid)) - 1u) & 0x55555555u;
+      if (rowmask) valid &= rowmask[t * 32 + w];
+      const uint32_t lo = word & 0x55555555u;
+      const uint32_t hi = (word >> 1) & 0x55555555u;
+      const int c_miss = __popc(lo & ~hi & valid);
+      const int c_het = __popc(hi & ~lo & valid);
+      const int c_hom = __popc(hi & lo & valid);
+      cnt += __popc(valid) - c_miss;
+      s1 += c_het + 2 * c_hom;
+      s2 += c_het + 4 * c_hom;
+      miss += c_miss;
+    }
+  }
+  if (j >= m.p) return;
+  const double dc = (double)cnt, d1 = (double)s1, d2 = (double)s2;
+  u[j] = cnt > 0 ? __ddiv_rn(d1, dc) : 0.0;
+  double vj = 0.0;
+  if (cnt >= 2) {
+    const double var = __ddiv_rn(__dsub_rn(d2, __ddiv_rn(__dmul_rn(d1, d1), dc)),
+                                 __dsub_rn(dc, 1.0));
+    vj = var > 0.0 ? __ddiv_rn(1.0, __dsqrt_rn(var)) : 0.0;
+  }
+  v[j] = vj;
+  if (missing_cnt) missing_cnt[j] = miss;
+}
+
+int launch_stats(const MatrixDesc& m, const uint32_t* d_rowmask, double* u, double* v,
+                 int32_t* d_missing_cnt, cudaStream_t s) {
+  if (m.p == 0) return 0;
+  const int threads = 256;
+  const int64_t blocks = (m.G * 32 + threads - 1) / threads;
+  stats_kernel<<<(unsigned)blocks, threads, 0, s>>>(m, d_rowmask, u, v, d_missing_cnt);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+// flags[g] = 1 when any SNP of group g has a missing genotype (lets the X^T r
+// kernel skip the missing-sum lookups for whole groups).
+__global__ void group_flags_kernel(int64_t p, int64_t G, const int32_t* __restrict__ miss,
+                                   uint8_t* __restrict__ flags) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  int any = 0;
+  for (int l = 0; l < 32; ++l) {
+    const int64_t j = g * 32 + l;
+    if (j < p && miss[j] > 0) any = 1;
+  }
+  flags[g] = (uint8_t)any;
+}
+
+int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_t* flags,
+                       cudaStream_t s) {
+  if (m.G == 0) return 0;
+  group_flags_kernel<<<(unsigned)((m.G + 255) / 256), 256, 0, s>>>(m.p, m.G, d_missing_cnt,
+                                                                    flags);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------- subset rows
+// dst holds m samples: sample i of dst = sample rows[i] of src.  One thread per
+// (SNP, dst word).  Padding codes past m stay zero.
+__global__ void subset_rows_kernel(MatrixDesc src, MatrixDesc dst, uint8_t* __restrict__ x,
+                                   const int64_t* __restrict__ rows) {
+  const int64_t words = dst.T * GI_TILE_WORDS;
+  const int64_t total = dst.p * words;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / words;
+    const int64_t wg = e - j * words;
+    uint32_t word = 0;
+    for (int s = 0; s < 16; ++s) {
+      const int64_t i = wg * 16 + s;
+      if (i >= dst.n) break;
+      const int64_t si = rows[i];
+      const uint32_t sw = *reinterpret_cast<const uint32_t*>(
+          src.x + word_offset(si >> 9, j, (int)((si >> 4) & 31), src.G));
+      word |= ((sw >> (2 * (si & 15))) & 3u) << (2 * s);
+    }
+    *reinterpret_cast<uint32_t*>(x + word_offset(wg >> 5, j, (int)(wg & 31), dst.G)) = word;
+  }
+}
+
+int launch_subset_rows(const MatrixDesc& src, const MatrixDesc& dst, uint8_t* x,
+                       const int64_t* d_rows, cudaStream_t s) {
+  if (dst.p == 0 || dst.n == 0) return 0;
+  subset_rows_kernel<<<grid_for(dst.p * dst.T * 32, 256), 256, 0, s>>>(src, dst, x, d_rows);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // namespace gi

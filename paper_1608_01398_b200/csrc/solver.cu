@@ -1,0 +1,494 @@
+// Device-side pieces of the IHT iteration other than X^T r and X_S w:
+// residual refresh, centring, covariate gradient, sup-norm reductions and the
+// hard-threshold top-k select.
+//
+// Reference: _refresh_state iht.py:183-191, iht_step iht.py:253-323,
+// top_k_indices iht.py:36-49 / hard_threshold :52-58.
+//
+// All reductions are deterministic: fixed grids write per-block partials and
+// the last block to finish (threadfence + atomic ticket) folds them in block
+// order, so repeated runs and any stream interleaving give identical bits.
+#include "common.cuh"
+
+namespace gi {
+
+constexpr int kRedBlocks = 296;
+constexpr int kRedThreads = 256;
+
+struct RedWs {
+  double* partials;        // kRedBlocks * 8
+  unsigned int* ticket;    // 1 counter, zero-initialised
+};
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__device__ __forceinline__ double warp_max(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// block-wide sum of NV values per thread; result valid in thread 0
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&x)[NV], double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    x[q] = warp_sum(x[q]);
+    if (lane == 0) sh[q * 32 + warp] = x[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += sh[q * 32 + w];
+      x[q] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// returns true in thread 0 of the last block to arrive
+__device__ __forceinline__ bool last_block(unsigned int* ticket) {
+  __shared__ bool is_last;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(ticket, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  return is_last;
+}
+
+// ---------------------------------------------------------------- residual
+// r_i = keep_i ? y_i - (fit_i + sum_l C[i, l] bcov[l]) : 0;
+// scal[0] = 0.5 * sum r^2 (loss), scal[1] = sum r / n_eff (centring mean).
+__global__ void residual_kernel(int64_t n, const double* __restrict__ y,
+                                const double* __restrict__ fit, const double* __restrict__ C,
+                                int c, const double* __restrict__ bcov,
+                                const uint8_t* __restrict__ keep, double n_eff,
+                                double* __restrict__ r, double* __restrict__ scal, RedWs ws) {
+  __shared__ double sh[64];
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double ri = 0.0;
+    if (!keep || keep[i]) {
+      double f = fit ? fit[i] : 0.0;
+      if (c > 0) {
+        double cb = 0.0;
+        for (int l = 0; l < c; ++l) cb = __dadd_rn(cb, __dmul_rn(C[i * c + l], bcov[l]));
+        f = fit ? __dadd_rn(f, cb) : cb;
+      }
+      ri = __dsub_rn(y[i], f);
+    }
+    r[i] = ri;
+    acc[0] += ri * ri;
+    acc[1] += ri;
+  }
+  block_sum<2>(acc, sh);
+  if (threadIdx.x == 0) {
+    ws.partials[blockIdx.x * 2] = acc[0];
+    ws.partials[blockIdx.x * 2 + 1] = acc[1];
+  }
+  if (last_block(ws.ticket) && threadIdx.x == 0) {
+    double s2 = 0.0, s1 = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      s2 += ws.partials[b * 2];
+      s1 += ws.partials[b * 2 + 1];
+    }
+    scal[0] = 0.5 * s2;
+    scal[1] = n_eff > 0.0 ? s1 / n_eff : 0.0;
+    *ws.ticket = 0u;
+  }
+}
+
+// rt_i = keep_i ? fp32(r_i - mean) : 0 over the padded length; scal[2] = sum rt.
+__global__ void center_kernel(int64_t n, int64_t n_pad, const double* __restrict__ r,
+                              const uint8_t* __restrict__ keep, double* __restrict__ scal,
+                              float* __restrict__ rt, RedWs ws) {
+  __shared__ double sh[32];
+  const double mean = scal[1];
+  double acc[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.0f;
+    if (i < n && (!keep || keep[i])) v = (float)(r[i] - mean);
+    rt[i] = v;
+    acc[0] += (double)v;
+  }
+  block_sum<1>(acc, sh);
+  if (threadIdx.x == 0) ws.partials[blockIdx.x] = acc[0];
+  if (last_block(ws.ticket) && threadIdx.x == 0) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += ws.partials[b];
+    scal[2] = s;
+    *ws.ticket = 0u;
+  }
+}
+
+// gcov[l] = -sum_i C[i, l] r_i  (covariate block of the gradient)
+__global__ void covgrad_kernel(int64_t n, const double* __restrict__ C, int c,
+                               const double* __restrict__ r, double* __restrict__ gcov,
+                               RedWs ws) {
+  __shared__ double sh[8 * 32];
+  double acc[8];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) acc[l] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = r[i];
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+      if (l < c) acc[l] += C[i * c + l] * ri;
+  }
+  block_sum<8>(acc, sh);
+  if (threadIdx.x == 0)
+    for (int l = 0; l < 8; ++l) ws.partials[blockIdx.x * 8 + l] = acc[l];
+  if (last_block(ws.ticket) && threadIdx.x == 0) {
+    for (int l = 0; l < c; ++l) {
+      double s = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) s += ws.partials[b * 8 + l];
+      gcov[l] = -s;
+    }
+    *ws.ticket = 0u;
+  }
+}
+
+// scal[slot] = max_j |x_j|
+__global__ void maxabs_kernel(int64_t m, const double* __restrict__ x, double* __restrict__ scal,
+                              int slot, RedWs ws) {
+  __shared__ double sh[32];
+  double mx = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mx = fmax(mx, fabs(x[i]));
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
+    ws.partials[blockIdx.x] = mx;
+  }
+  if (last_block(ws.ticket) && threadIdx.x == 0) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s = fmax(s, ws.partials[b]);
+    scal[slot] = s;
+    *ws.ticket = 0u;
+  }
+}
+
+// scal[slot] = sum_i x_i^2
+__global__ void sumsq_kernel(int64_t m, const double* __restrict__ x, double* __restrict__ scal,
+                             int slot, RedWs ws) {
+  __shared__ double sh[32];
+  double acc[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc[0] += x[i] * x[i];
+  block_sum<1>(acc, sh);
+  if (threadIdx.x == 0) ws.partials[blockIdx.x] = acc[0];
+  if (last_block(ws.ticket) && threadIdx.x == 0) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += ws.partials[b];
+    scal[slot] = s;
+    *ws.ticket = 0u;
+  }
+}
+
+// out = x + C @ w (length n; C row-major (n, c)); used for X_S w + C w_cov
+__global__ void add_cov_kernel(int64_t n, const double* __restrict__ C, int c,
+                               const double* __restrict__ w, double* __restrict__ x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double cb = 0.0;
+    for (int l = 0; l < c; ++l) cb = __dadd_rn(cb, __dmul_rn(C[i * c + l], w[l]));
+    x[i] = __dadd_rn(x[i], cb);
+  }
+}
+
+static int red_grid(int64_t m) {
+  int64_t g = (m + kRedThreads - 1) / kRedThreads;
+  if (g > kRedBlocks) g = kRedBlocks;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int launch_residual(int64_t n, const double* y, const double* fit, const double* C, int c,
+                    const double* bcov, const uint8_t* keep, double n_eff, double* r,
+                    double* scal, double* partials, unsigned int* ticket, cudaStream_t s) {
+  RedWs ws{partials, ticket};
+  residual_kernel<<<red_grid(n), kRedThreads, 0, s>>>(n, y, fit, C, c, bcov, keep, n_eff, r,
+                                                     scal, ws);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_center(int64_t n, int64_t n_pad, const double* r, const uint8_t* keep, double* scal,
+                  float* rt, double* partials, unsigned int* ticket, cudaStream_t s) {
+  RedWs ws{partials, ticket};
+  center_kernel<<<red_grid(n_pad), kRedThreads, 0, s>>>(n, n_pad, r, keep, scal, rt, ws);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_covgrad(int64_t n, const double* C, int c, const double* r, double* gcov,
+                   double* partials, unsigned int* ticket, cudaStream_t s) {
+  if (c <= 0) return 0;
+  if (c > 8) {
+    gi_set_error("at most 8 covariate columns are supported on the device path");
+    return -1;
+  }
+  RedWs ws{partials, ticket};
+  covgrad_kernel<<<red_grid(n), kRedThreads, 0, s>>>(n, C, c, r, gcov, ws);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_maxabs(int64_t m, const double* x, double* scal, int slot, double* partials,
+                  unsigned int* ticket, cudaStream_t s) {
+  RedWs ws{partials, ticket};
+  maxabs_kernel<<<red_grid(m), kRedThreads, 0, s>>>(m, x, scal, slot, ws);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_sumsq(int64_t m, const double* x, double* scal, int slot, double* partials,
+                 unsigned int* ticket, cudaStream_t s) {
+  RedWs ws{partials, ticket};
+  sumsq_kernel<<<red_grid(m), kRedThreads, 0, s>>>(m, x, scal, slot, ws);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_add_cov(int64_t n, const double* C, int c, const double* w, double* x,
+                   cudaStream_t s) {
+  if (c <= 0 || n == 0) return 0;
+  add_cov_kernel<<<red_grid(n), kRedThreads, 0, s>>>(n, C, c, w, x);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+// ---------------------------------------------------------------- top-k
+// Exact k largest under the total order (key desc, index asc) -- the
+// reference's "ties go to the lower index" rule (iht.py:44-49).  Keys are the
+// bit patterns of |value| (non-negative doubles order like uint64), stored +1
+// so that 0 marks an empty slot.  Radix select over 8 key digits and 4 digits
+// of ~index (MSB first), stopping as soon as the boundary bin is taken whole.
+constexpr int kTopkChunk = 4096;
+constexpr int kTopkThreads = 512;
+
+template <typename Get>
+__device__ void block_select(int64_t m, int64_t k, Get get, uint64_t& thr_key,
+                             uint32_t& thr_sec) {
+  __shared__ unsigned int hist[256];
+  __shared__ uint64_t s_key, s_kmask;
+  __shared__ uint32_t s_sec, s_smask;
+  __shared__ int64_t s_kk;
+  __shared__ int s_done;
+  if (threadIdx.x == 0) {
+    s_key = 0;
+    s_kmask = 0;
+    s_sec = 0;
+    s_smask = 0;
+    s_kk = k;
+    s_done = 0;
+  }
+  __syncthreads();
+  for (int d = 0; d < 12; ++d) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0u;
+    __syncthreads();
+    const uint64_t pk = s_key, mk = s_kmask;
+    const uint32_t ps = s_sec, ms = s_smask;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      uint64_t key;
+      uint32_t sec;
+      get(i, key, sec);
+      if ((key & mk) == pk && (sec & ms) == ps) {
+        const unsigned digit = d < 8 ? (unsigned)((key >> (56 - 8 * d)) & 255u)
+                                     : (unsigned)((sec >> (24 - 8 * (d - 8))) & 255u);
+        atomicAdd(&hist[digit], 1u);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t need = s_kk;
+      int bin = 255;
+      for (; bin >= 0; --bin) {
+        if ((int64_t)hist[bin] >= need) break;
+        need -= hist[bin];
+      }
+      if (bin < 0) bin = 0;  // fewer elements than k: everything is taken
+      if (d < 8) {
+        s_key |= (uint64_t)bin << (56 - 8 * d);
+        s_kmask |= (uint64_t)255u << (56 - 8 * d);
+      } else {
+        s_sec |= (uint32_t)bin << (24 - 8 * (d - 8));
+        s_smask |= 255u << (24 - 8 * (d - 8));
+      }
+      s_kk = need;
+      if ((int64_t)hist[bin] == need) s_done = 1;
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
+  thr_key = s_key;
+  thr_sec = s_sec;
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool ge_thr(uint64_t key, uint32_t sec, uint64_t tk, uint32_t ts) {
+  return key > tk || (key == tk && sec >= ts);
+}
+
+// mode 0: value = g_j; mode 1: value = beta_j - mu * g_j.  key = |value|.
+__device__ __forceinline__ double topk_value(int mode, const double* beta, const double* g,
+                                             double mu, int64_t j) {
+  if (mode == 0) return g[j];
+  return __dsub_rn(beta[j], __dmul_rn(mu, g[j]));
+}
+
+__device__ __forceinline__ uint64_t key_of(double val) {
+  return (uint64_t)__double_as_longlong(fabs(val)) + 1ull;
+}
+
+// One block per chunk of kTopkChunk elements; writes k candidate slots
+// (cand_key = 0 marks an unused slot).
+__global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(
+    int64_t p, int64_t k, int mode, const double* __restrict__ beta,
+    const double* __restrict__ g, double mu, int64_t idx_base, uint64_t* __restrict__ cand_key,
+    int64_t* __restrict__ cand_idx, double* __restrict__ cand_val) {
+  __shared__ uint64_t keys[kTopkChunk];
+  __shared__ unsigned int s_pos;
+  const int64_t lo = (int64_t)blockIdx.x * kTopkChunk;
+  const int64_t hi = lo + kTopkChunk < p ? lo + kTopkChunk : p;
+  const int64_t m = hi - lo;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x)
+    keys[i] = key_of(topk_value(mode, beta, g, mu, lo + i));
+  if (threadIdx.x == 0) s_pos = 0u;
+  __syncthreads();
+  uint64_t tk;
+  uint32_t ts;
+  auto get = [&](int64_t i, uint64_t& key, uint32_t& sec) {
+    key = keys[i];
+    sec = ~(uint32_t)(idx_base + lo + i);
+  };
+  const int64_t kk = k < m ? k : m;
+  if (kk < m) {
+    block_select(m, kk, get, tk, ts);
+  } else {
+    tk = 1;
+    ts = 0;  // take everything
+  }
+  uint64_t* ok = cand_key + (int64_t)blockIdx.x * k;
+  int64_t* oi = cand_idx + (int64_t)blockIdx.x * k;
+  double* ov = cand_val + (int64_t)blockIdx.x * k;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    uint64_t key;
+    uint32_t sec;
+    get(i, key, sec);
+    if (ge_thr(key, sec, tk, ts)) {
+      const unsigned pos = atomicAdd(&s_pos, 1u);
+      ok[pos] = key;
+      oi[pos] = idx_base + lo + i;
+      ov[pos] = topk_value(mode, beta, g, mu, lo + i);
+    }
+  }
+  __syncthreads();
+  for (int64_t s = s_pos + threadIdx.x; s < k; s += blockDim.x) {
+    ok[s] = 0;
+    oi[s] = -1;
+    ov[s] = 0.0;
+  }
+}
+
+// Single block: exact top-k over `mc` candidates -> out (unordered) + count.
+__global__ void __launch_bounds__(1024) topk_merge_kernel(
+    int64_t mc, int64_t k, const uint64_t* __restrict__ cand_key,
+    const int64_t* __restrict__ cand_idx, const double* __restrict__ cand_val,
+    int64_t* __restrict__ out_idx, double* __restrict__ out_val, uint64_t* __restrict__ out_key,
+    int64_t* __restrict__ out_count) {
+  __shared__ unsigned int s_pos;
+  if (threadIdx.x == 0) s_pos = 0u;
+  __syncthreads();
+  auto get = [&](int64_t i, uint64_t& key, uint32_t& sec) {
+    key = cand_key[i];
+    sec = ~(uint32_t)cand_idx[i];
+  };
+  uint64_t tk;
+  uint32_t ts;
+  block_select(mc, k, get, tk, ts);
+  if (tk == 0) tk = 1;  // never take empty slots
+  for (int64_t i = threadIdx.x; i < mc; i += blockDim.x) {
+    uint64_t key;
+    uint32_t sec;
+    get(i, key, sec);
+    if (ge_thr(key, sec, tk, ts)) {
+      const unsigned pos = atomicAdd(&s_pos, 1u);
+      if (pos < k) {
+        out_idx[pos] = cand_idx[i];
+        out_val[pos] = cand_val[i];
+        if (out_key) out_key[pos] = key;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *out_count = s_pos < k ? (int64_t)s_pos : k;
+}
+
+int64_t topk_blocks(int64_t p) { return (p + kTopkChunk - 1) / kTopkChunk; }
+
+int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double* g, double mu,
+                int64_t idx_base, uint64_t* cand_key, int64_t* cand_idx, double* cand_val,
+                int64_t* out_idx, double* out_val, uint64_t* out_key, int64_t* out_count,
+                cudaStream_t s) {
+  if (k <= 0 || p <= 0) {
+    GI_CUDA_TRY(cudaMemsetAsync(out_count, 0, sizeof(int64_t), s));
+    return 0;
+  }
+  const int64_t nb = topk_blocks(p);
+  topk_local_kernel<<<(unsigned)nb, kTopkThreads, 0, s>>>(p, k, mode, beta, g, mu, idx_base,
+                                                          cand_key, cand_idx, cand_val);
+  GI_LAUNCH_CHECK();
+  topk_merge_kernel<<<1, 1024, 0, s>>>(nb * k, k, cand_key, cand_idx, cand_val, out_idx,
+                                       out_val, out_key, out_count);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+// dense beta update: beta[idx[t]] = val[t]
+__global__ void scatter_kernel(int64_t k, const int64_t* __restrict__ idx,
+                               const double* __restrict__ val, double* __restrict__ beta) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < k) beta[idx[t]] = val[t];
+}
+
+__global__ void gather_kernel(int64_t k, const int64_t* __restrict__ idx,
+                              const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < k) dst[t] = src[idx[t]];
+}
+
+int launch_scatter(int64_t k, const int64_t* idx, const double* val, double* beta,
+                   cudaStream_t s) {
+  if (k <= 0) return 0;
+  scatter_kernel<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, idx, val, beta);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_gather(int64_t k, const int64_t* idx, const double* src, double* dst,
+                  cudaStream_t s) {
+  if (k <= 0) return 0;
+  gather_kernel<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, idx, src, dst);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // namespace gi

@@ -1,0 +1,112 @@
+"""SNP-block sharding across GPUs (one process per GPU, torch.distributed).
+
+The genotype matrix is split into contiguous SNP blocks, one per rank
+(SURVEY.md section 8(e)).  Every rank runs the same IHT control flow on
+identical reduced values, so all ranks take identical branches.  The only data
+exchanged per iteration are n-length partial products (X_S w summed across
+shards: NCCL all-reduce on device buffers) and the k-candidate top-k lists
+(all-gather), plus a few scalars.
+
+``LocalComm`` is the single-process communicator; ``TorchComm`` wraps the
+default torch.distributed process group (NCCL across GPUs; gloo for the CPU
+tests).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_range(p: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous SNP block [j0, j1) of ``rank``; blocks differ by at most one SNP."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("invalid world size / rank")
+    base, extra = divmod(int(p), int(world))
+    j0 = rank * base + min(rank, extra)
+    return j0, j0 + base + (1 if rank < extra else 0)
+
+
+class LocalComm:
+    world = 1
+    rank = 0
+
+    def allreduce_sum_(self, tensor):
+        return tensor
+
+    def allreduce_max(self, value: float) -> float:
+        return float(value)
+
+    def allreduce_sum_host(self, array: np.ndarray) -> np.ndarray:
+        return np.asarray(array, dtype=np.float64)
+
+    def allgather_host(self, array: np.ndarray) -> list:
+        return [np.asarray(array)]
+
+
+class TorchComm:
+    """Collectives on the default process group.  Device buffers go straight to
+    NCCL; with the gloo backend (CPU tests) CUDA buffers are staged on the host."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.backend = dist.get_backend(group)
+
+    def _device(self):
+        import torch
+
+        if self.backend == "nccl":
+            return torch.device("cuda", torch.cuda.current_device())
+        return torch.device("cpu")
+
+    def allreduce_sum_(self, tensor):
+        if self.backend != "nccl" and tensor.is_cuda:
+            host = tensor.cpu()
+            self.dist.all_reduce(host, group=self.group)
+            tensor.copy_(host)
+        else:
+            self.dist.all_reduce(tensor, group=self.group)
+        return tensor
+
+    def allreduce_max(self, value: float) -> float:
+        import torch
+
+        t = torch.tensor([float(value)], dtype=torch.float64, device=self._device())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def allreduce_sum_host(self, array: np.ndarray) -> np.ndarray:
+        import torch
+
+        t = torch.as_tensor(np.asarray(array, dtype=np.float64)).to(self._device())
+        self.dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    def allgather_host(self, array: np.ndarray) -> list:
+        import torch
+
+        t = torch.as_tensor(np.ascontiguousarray(array)).to(self._device())
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy() for o in out]
+
+
+def merge_topk(keys: np.ndarray, idx: np.ndarray, vals: np.ndarray, k: int):
+    """Global top-k from per-shard candidate lists under (|value| desc, index asc).
+
+    ``keys`` are the uint64 bit patterns of |value| plus one (0 = empty slot),
+    exactly as gi_dev_topk emits them; each shard's list is already its exact
+    local top-k under the same order, so their union contains the global one.
+    Returns indices sorted ascending and the matching values.
+    """
+    keys = np.asarray(keys, dtype=np.uint64)
+    live = keys != 0
+    keys, idx, vals = keys[live], np.asarray(idx)[live], np.asarray(vals)[live]
+    order = np.lexsort((idx, ~keys))  # key descending, then index ascending
+    take = order[:k]
+    sel = np.argsort(idx[take], kind="stable")
+    return idx[take][sel].astype(np.int64), vals[take][sel]

@@ -1,0 +1,319 @@
+"""Device state and fused phases of one IHT fit on one SNP shard.
+
+The IHT control flow (iht.py) is the reference's, step for step; everything
+O(n), O(p) or O(n p) it needs runs here as libgenoiht_cuda.so kernels on the
+shard's GPU, with only O(k) values crossing to the host once per phase:
+
+    refresh      X_S w (+ all-reduce) -> r = y - X_S w - C b_cov, loss, centred
+                 fp32 residual, g = -X^T r (lookup-table kernel), g_cov, max|g|,
+                 g on the support                       (iht.py:183-191, :257-261)
+    image        ||X_idx w + C w_cov||^2                 (iht.py:238-241, :295-296)
+    top-k        k largest |beta - mu g| or |g|          (iht.py:36-58, :228, :280)
+
+torch is used only to allocate device buffers and to hand NCCL the n-length
+partial products; all arithmetic is in the CUDA kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from ._native import check, lib
+
+_SCAL = 8  # device scalar slots: 0 loss, 1 mean(r), 2 sum(rt), 3 max|g|, 4 image sumsq
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class Genotypes:
+    """What the engine needs to know about the genotype operand of a view.
+
+    handle  gi_matrix* of the (local shard of the) packed matrix
+    n_full  samples stored on the device (rows outside ``rows`` are ignored)
+    rows    sample subset the view stands for (None = all), e.g. CV training rows
+    u, v    device stats to standardise with (None = the handle's own)
+    j_base  global index of local SNP 0;  p_local / p_global  shard / total SNPs
+    """
+
+    def __init__(self, matrix, rows=None, u=None, v=None, j_base=0, p_global=None, comm=None):
+        from .dist import LocalComm
+
+        self.matrix = matrix
+        self.handle = matrix.handle
+        self.device = matrix.device
+        self.n_full = matrix.n
+        self.rows = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+        self.u = u
+        self.v = v
+        self.j_base = int(j_base)
+        self.p_local = matrix.p
+        self.p_global = matrix.p if p_global is None else int(p_global)
+        self.comm = comm if comm is not None else LocalComm()
+
+
+class DeviceEngine:
+    def __init__(self, geno: Genotypes, y: np.ndarray, cov: np.ndarray | None, kmax: int):
+        torch = _torch()
+        _native.require_device(geno.device)
+        self.torch = torch
+        self.geno = geno
+        self.comm = geno.comm
+        self.dev = torch.device("cuda", geno.device)
+        self.h = geno.handle
+        self.n = geno.n_full
+        self.p = geno.p_local
+        self.c = 0 if cov is None else int(cov.shape[1])
+        self.kmax = max(1, int(kmax))
+        self.n_pad = int(lib().gi_padded_samples(self.h))
+        f64, dev = torch.float64, self.dev
+        with torch.cuda.device(self.dev):
+            self.stream = torch.cuda.current_stream(self.dev)
+        self.s = ctypes.c_void_p(self.stream.cuda_stream)
+
+        y_full = np.zeros(self.n)
+        keep = None
+        if geno.rows is None:
+            y_full[:] = y
+            self.n_eff = float(self.n)
+        else:
+            y_full[geno.rows] = y
+            keep = np.zeros(self.n, np.uint8)
+            keep[geno.rows] = 1
+            self.n_eff = float(geno.rows.size)
+        self.y = torch.as_tensor(y_full, dtype=f64).to(dev)
+        self.keep = None if keep is None else torch.as_tensor(keep).to(dev)
+        if self.c:
+            c_full = np.zeros((self.n, self.c))
+            if geno.rows is None:
+                c_full[:] = cov
+            else:
+                c_full[geno.rows] = cov
+            self.C = torch.as_tensor(np.ascontiguousarray(c_full), dtype=f64).to(dev)
+        else:
+            self.C = None
+        self.r = torch.zeros(self.n, dtype=f64, device=dev)
+        self.fit = torch.zeros(self.n, dtype=f64, device=dev)
+        self.img = torch.zeros(self.n, dtype=f64, device=dev)
+        self.rt = torch.zeros(self.n_pad, dtype=torch.float32, device=dev)
+        self.g = torch.zeros(max(self.p, 1), dtype=f64, device=dev)
+        self.beta = torch.zeros(max(self.p, 1), dtype=f64, device=dev)
+        self.cvec = torch.zeros(max(self.c, 1) * 2, dtype=f64, device=dev)  # bcov | gcov
+        self.scal = torch.zeros(_SCAL, dtype=f64, device=dev)
+        self.partials = torch.zeros(int(lib().gi_red_partials()), dtype=f64, device=dev)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+        slots = int(lib().gi_topk_slots(max(self.p, 1), self.kmax))
+        self.ckey = torch.zeros(slots, dtype=torch.int64, device=dev)
+        self.cidx = torch.zeros(slots, dtype=torch.int64, device=dev)
+        self.cval = torch.zeros(slots, dtype=f64, device=dev)
+        self.oidx = torch.zeros(self.kmax, dtype=torch.int64, device=dev)
+        self.oval = torch.zeros(self.kmax, dtype=f64, device=dev)
+        self.okey = torch.zeros(self.kmax, dtype=torch.int64, device=dev)
+        self.ocnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._kbuf = 0
+        self._ensure_kbuf(max(2 * self.kmax, 64))
+        # pinned staging for the small host<->device traffic of each phase
+        self.h_out = torch.zeros(_SCAL + 2 * self.c + 4 * self.kmax + 4, dtype=f64).pin_memory()
+        self.u_ptr = None if geno.u is None else geno.u.data_ptr()
+        self.v_ptr = None if geno.v is None else geno.v.data_ptr()
+        self.kernel_launches = 0
+
+    # ------------------------------------------------------------- helpers
+    def _ensure_kbuf(self, k):
+        if k <= self._kbuf:
+            return
+        torch = self.torch
+        k = max(k, 2 * self._kbuf)
+        self.d_idx = torch.zeros(k, dtype=torch.int64, device=self.dev)
+        self.d_w = torch.zeros(k, dtype=torch.float64, device=self.dev)
+        self.h_idx = torch.zeros(k, dtype=torch.int64).pin_memory()
+        self.h_w = torch.zeros(k, dtype=torch.float64).pin_memory()
+        self._kbuf = k
+
+    def _upload_sparse(self, idx_local: np.ndarray, w: np.ndarray) -> int:
+        k = int(idx_local.size)
+        if k == 0:
+            return 0
+        self._ensure_kbuf(k)
+        self.h_idx.numpy()[:k] = idx_local
+        self.h_w.numpy()[:k] = w
+        self.d_idx[:k].copy_(self.h_idx[:k], non_blocking=True)
+        self.d_w[:k].copy_(self.h_w[:k], non_blocking=True)
+        return k
+
+    def _sync(self):
+        self.stream.synchronize()
+
+    def local_part(self, idx_global: np.ndarray, w: np.ndarray):
+        """Entries of a global sparse vector owned by this shard (local indices)."""
+        idx_global = np.asarray(idx_global, dtype=np.int64)
+        if self.comm.world == 1 and self.geno.j_base == 0:
+            return idx_global, np.asarray(w, dtype=np.float64)
+        lo, hi = self.geno.j_base, self.geno.j_base + self.p
+        sel = (idx_global >= lo) & (idx_global < hi)
+        return idx_global[sel] - lo, np.asarray(w, dtype=np.float64)[sel]
+
+    def _ax_into(self, out, idx_global, w):
+        idx_l, w_l = self.local_part(idx_global, w)
+        k = self._upload_sparse(idx_l, w_l)
+        P = _native.ptr
+        check(lib().gi_dev_ax(self.h, self.u_ptr, self.v_ptr, P(self.d_idx), P(self.d_w), k,
+                              P(out), 0, self.s))
+        self.kernel_launches += 1 if k else 0
+        if self.comm.world > 1:
+            self.comm.allreduce_sum_(out)
+
+    # --------------------------------------------------------------- phases
+    def set_beta(self, old_idx, new_idx, new_w):
+        """Dense device beta: zero the old support, write the new one."""
+        P = _native.ptr
+        old_l, _ = self.local_part(old_idx, np.zeros(len(old_idx)))
+        if old_l.size:
+            k = self._upload_sparse(old_l, np.zeros(old_l.size))
+            check(lib().gi_dev_scatter(k, P(self.d_idx), P(self.d_w), P(self.beta), self.s))
+            self.kernel_launches += 1
+        new_l, w_l = self.local_part(new_idx, new_w)
+        if new_l.size:
+            k = self._upload_sparse(new_l, w_l)
+            check(lib().gi_dev_scatter(k, P(self.d_idx), P(self.d_w), P(self.beta), self.s))
+            self.kernel_launches += 1
+
+    def refresh(self, support, weights, bcov):
+        """r, loss and the full gradient at (support, weights, bcov).
+
+        Returns (loss, max|g_gen| over all shards, g_cov (c,), g on support)."""
+        P = _native.ptr
+        L = lib()
+        has_fit = len(support) > 0
+        if has_fit:
+            self._ax_into(self.fit, support, weights)
+        if self.c:
+            self.h_out.numpy()[: self.c] = bcov
+            self.cvec[: self.c].copy_(self.h_out[: self.c], non_blocking=True)
+        cptr = P(self.cvec)
+        gcov_ptr = cptr + 8 * self.c if self.c else None
+        check(L.gi_dev_residual(self.n, P(self.y), P(self.fit) if has_fit else None,
+                                P(self.C) if self.c else None, self.c, cptr if self.c else None,
+                                P(self.keep) if self.keep is not None else None, self.n_eff,
+                                P(self.r), P(self.scal), P(self.partials), P(self.ticket),
+                                self.s))
+        check(L.gi_dev_center(self.n, self.n_pad, P(self.r),
+                              P(self.keep) if self.keep is not None else None, P(self.scal),
+                              P(self.rt), P(self.partials), P(self.ticket), self.s))
+        if self.p:
+            check(L.gi_dev_aty_fast(self.h, self.u_ptr, self.v_ptr, P(self.rt),
+                                    P(self.scal) + 16, -1.0, P(self.g), self.s))
+            check(L.gi_dev_maxabs(self.p, P(self.g), P(self.scal), 3, P(self.partials),
+                                  P(self.ticket), self.s))
+        if self.c:
+            check(L.gi_dev_covgrad(self.n, P(self.C), self.c, P(self.r), gcov_ptr,
+                                   P(self.partials), P(self.ticket), self.s))
+        self.kernel_launches += 2 + (2 if self.p else 0) + (1 if self.c else 0)
+        sup_l, _ = self.local_part(support, np.zeros(len(support)))
+        ks = int(sup_l.size)
+        if ks:
+            self._upload_sparse(sup_l, np.zeros(ks))
+            check(L.gi_dev_gather(ks, P(self.d_idx), P(self.g), P(self.oval), self.s))
+            self.kernel_launches += 1
+        ho = self.h_out
+        ho[:_SCAL].copy_(self.scal, non_blocking=True)
+        if self.c:
+            ho[_SCAL:_SCAL + self.c].copy_(self.cvec[self.c:2 * self.c], non_blocking=True)
+        if ks:
+            ho[_SCAL + self.c:_SCAL + self.c + ks].copy_(self.oval[:ks], non_blocking=True)
+        self._sync()
+        hv = ho.numpy()
+        loss = float(hv[0])
+        gmax = float(hv[3]) if self.p else 0.0
+        gcov = hv[_SCAL:_SCAL + self.c].copy()
+        g_loc = hv[_SCAL + self.c:_SCAL + self.c + ks].copy()
+        if self.comm.world > 1:
+            gmax = self.comm.allreduce_max(gmax)
+            g_sup = self._assemble(support, g_loc)
+        else:
+            g_sup = g_loc
+        return loss, gmax, gcov, g_sup
+
+    def _assemble(self, idx_global, local_vals):
+        """Values of a global index list whose entries are spread over shards."""
+        idx_global = np.asarray(idx_global, dtype=np.int64)
+        full = np.zeros(idx_global.size)
+        lo, hi = self.geno.j_base, self.geno.j_base + self.p
+        sel = (idx_global >= lo) & (idx_global < hi)
+        full[sel] = local_vals
+        return self.comm.allreduce_sum_host(full)
+
+    def image_sumsq(self, idx, w, wcov) -> float:
+        """|| X_idx w + C wcov ||^2 (rows outside the view contribute 0)."""
+        P = _native.ptr
+        L = lib()
+        self._ax_into(self.img, idx, w)
+        if wcov is not None and self.c:
+            self.h_out.numpy()[: self.c] = wcov
+            self.cvec[: self.c].copy_(self.h_out[: self.c], non_blocking=True)
+            check(L.gi_dev_add_cov(self.n, P(self.C), self.c, P(self.cvec), P(self.img), self.s))
+            self.kernel_launches += 1
+        if self.keep is not None:
+            self.img.mul_(self.keep)
+        check(L.gi_dev_sumsq(self.n, P(self.img), P(self.scal), 4, P(self.partials),
+                             P(self.ticket), self.s))
+        self.kernel_launches += 1
+        self.h_out[4:5].copy_(self.scal[4:5], non_blocking=True)
+        self._sync()
+        return float(self.h_out.numpy()[4])
+
+    def topk(self, mode: int, mu: float, k: int):
+        """Global top-k (sorted indices, values) of |g| (mode 0) or |beta - mu g| (mode 1)."""
+        from .dist import merge_topk
+
+        P = _native.ptr
+        k_eff = min(int(k), self.kmax)
+        if self.p == 0 or k_eff <= 0:
+            keys = np.zeros(0, np.uint64)
+            idx = np.zeros(0, np.int64)
+            vals = np.zeros(0)
+        else:
+            check(lib().gi_dev_topk(self.p, k_eff, mode, P(self.beta), P(self.g), float(mu),
+                                    self.geno.j_base, P(self.ckey), P(self.cidx), P(self.cval),
+                                    P(self.oidx), P(self.oval), P(self.okey), P(self.ocnt),
+                                    self.s))
+            self.kernel_launches += 2
+            ho = self.h_out
+            base = _SCAL + 2 * self.c
+            ho[base:base + k_eff].copy_(self.oidx[:k_eff].view(self.torch.float64),
+                                        non_blocking=True)
+            ho[base + k_eff:base + 2 * k_eff].copy_(self.oval[:k_eff], non_blocking=True)
+            ho[base + 2 * k_eff:base + 3 * k_eff].copy_(self.okey[:k_eff].view(self.torch.float64),
+                                                       non_blocking=True)
+            ho[base + 3 * k_eff:base + 3 * k_eff + 1].copy_(self.ocnt.view(self.torch.float64),
+                                                           non_blocking=True)
+            self._sync()
+            hv = ho.numpy()
+            cnt = int(hv[base + 3 * k_eff:base + 3 * k_eff + 1].view(np.int64)[0])
+            idx = hv[base:base + cnt].view(np.int64).copy()
+            vals = hv[base + k_eff:base + k_eff + cnt].copy()
+            keys = hv[base + 2 * k_eff:base + 2 * k_eff + cnt].view(np.uint64).copy()
+        if self.comm.world > 1:
+            pad = np.zeros(k_eff, np.uint64)
+            pad_i = np.full(k_eff, -1, np.int64)
+            pad_v = np.zeros(k_eff)
+            pad[: keys.size], pad_i[: idx.size], pad_v[: vals.size] = keys, idx, vals
+            ks = np.concatenate(self.comm.allgather_host(pad.view(np.int64))).view(np.uint64)
+            ii = np.concatenate(self.comm.allgather_host(pad_i))
+            vv = np.concatenate(self.comm.allgather_host(pad_v))
+            return merge_topk(ks, ii, vv, k_eff)
+        return merge_topk(keys, idx, vals, k_eff)
+
+    def gradient(self) -> np.ndarray:
+        """Local genetic gradient (host copy)."""
+        return self.g[: self.p].cpu().numpy().copy()
+
+    def residuals(self) -> np.ndarray:
+        r = self.r.cpu().numpy()
+        return r if self.geno.rows is None else r[self.geno.rows].copy()

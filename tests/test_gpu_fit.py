@@ -1,0 +1,107 @@
+"""GPU parity of the device IHT loop and cross-validation against the
+reference (golden vectors) and the oracle.
+
+North-star parity bar: identical support and iteration count (and CV k_best /
+MSE grid ranking), beta and loss within 1e-6 relative.
+"""
+import numpy as np
+import pytest
+
+import golden_io
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-6  # north star: beta and loss within 1e-6 relative
+
+
+def _gi():
+    import paper_1608_01398_b200 as gi
+    return gi
+
+
+def _view(case, codes):
+    gi = _gi()
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    cov = gi.CovariateBlock.build(None, n=case["n"]) if case["intercept"] else None
+    return gi.StandardizedView(m, cov)
+
+
+def _assert_fit(res, support, weights, covar, loss_trace, iterations, reason):
+    np.testing.assert_array_equal(res.model.support, support)
+    assert res.iterations == iterations
+    assert res.reason == reason
+    np.testing.assert_allclose(res.model.weights, weights, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(res.model.covar, covar, rtol=RTOL, atol=1e-12)
+    np.testing.assert_allclose(res.loss_trace, loss_trace, rtol=RTOL, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", sorted(golden_io.load("fits")))
+def test_fit_matches_reference(name):
+    case = golden_io.load("fits")[name]
+    codes = golden_io.codes_for(case)
+    gi = _gi()
+    res = gi.fit(_view(case, codes), case["y"], gi.IhtConfig(k=int(case["k"])))
+    _assert_fit(res, case["support"], case["weights"], case["covar"], case["loss_trace"],
+                case["iterations"], case["reason"])
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fit_matches_oracle_random(seed):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(60, 900))
+    p = int(rng.integers(50, 3000))
+    miss = float(rng.choice([0.0, 0.02, 0.1]))
+    codes = oracle.random_codes(n, p, seed=seed, missing_rate=miss)
+    k = int(rng.integers(1, 12))
+    covar = rng.standard_normal((n, 2)) if seed % 3 == 0 else None
+    gi = _gi()
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    block = gi.CovariateBlock.build(covar, n=n, add_intercept=seed % 4 != 1) \
+        if (covar is not None or seed % 4 != 1) else None
+    view = gi.StandardizedView(m, block)
+    ref = oracle.OracleView(oracle.OraclePacked.from_codes(codes),
+                            None if block is None else block.values)
+    support = np.sort(rng.choice(p, min(k, 5), replace=False))
+    y = ref.geno.ax_columns(support, rng.standard_normal(support.size)) + rng.normal(0, 0.2, n)
+    want = oracle.fit(ref, y, k)
+    got = gi.fit(view, y, gi.IhtConfig(k=k))
+    _assert_fit(got, want.support, want.weights, want.covar, want.loss_trace, want.iterations,
+                want.reason)
+
+
+def test_warm_start_and_collapse():
+    gi = _gi()
+    codes = oracle.random_codes(120, 40, seed=4, missing_rate=0.0)
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    view = gi.StandardizedView(m, None)
+    ref = oracle.OracleView(oracle.OraclePacked.from_codes(codes), None)
+    y = ref.geno.ax_columns(np.array([3]), np.array([2.0]))
+    warm = gi.SparseModel.from_parts([11], [1.0], np.zeros(0), k=1, p=40)
+    got = gi.fit(view, y, gi.IhtConfig(k=1, c_omega=0.99, max_backtracks=0), warm=warm)
+    want = oracle.fit(ref, y, 1, c_omega=0.99, max_backtracks=0,
+                      warm=(np.array([11]), np.array([1.0]), np.zeros(0)))
+    assert got.reason == want.reason
+    assert got.iterations == want.iterations
+    got2 = gi.fit(view, y, gi.IhtConfig(k=2), warm=warm)
+    want2 = oracle.fit(ref, y, 2, warm=(np.array([11]), np.array([1.0]), np.zeros(0)))
+    _assert_fit(got2, want2.support, want2.weights, want2.covar, want2.loss_trace,
+                want2.iterations, want2.reason)
+
+
+@pytest.mark.parametrize("name", sorted(golden_io.load("cv")))
+def test_cv_matches_reference(name):
+    case = golden_io.load("cv")[name]
+    codes = golden_io.codes_for(case)
+    gi = _gi()
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=case["n"]))
+    plan = gi.CvPlan.build(case["n"], case["q"], case["path"], seed=case["fold_seed"])
+    np.testing.assert_array_equal(plan.fold_labels, case["labels"])
+    rep = gi.cv_iht(view, case["y"], plan, gi.IhtConfig(k=int(case["path"].max())),
+                    std_mode=case["std_mode"], warm_start=bool(case["warm"]))
+    assert rep.k_best == case["k_best"]
+    np.testing.assert_allclose(rep.mse, case["mse"], rtol=1e-5, atol=1e-9)
+    np.testing.assert_array_equal(rep.final_model.support, case["final_support"])
+    np.testing.assert_allclose(rep.final_model.weights, case["final_weights"], rtol=RTOL)
+    np.testing.assert_allclose(rep.final_model.covar, case["final_covar"], rtol=RTOL, atol=1e-12)

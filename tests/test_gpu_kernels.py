@@ -1,0 +1,119 @@
+"""GPU parity of the packed-genotype kernels against the oracle and the
+reference's golden vectors (bit-exact where the reference is bit-reproducible).
+"""
+import numpy as np
+import pytest
+
+import golden_io
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _gm():
+    import paper_1608_01398_b200 as gi
+    return gi
+
+
+def _pair(case):
+    codes = golden_io.codes_for(case)
+    ref = oracle.OraclePacked.from_codes(codes)
+    assert golden_io.sha(ref.data) == case["data_sha"]
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    return codes, ref, dev
+
+
+@pytest.mark.parametrize("name", sorted(golden_io.load("kernels")))
+def test_kernels_bit_exact_vs_reference(name):
+    case = golden_io.load("kernels")[name]
+    codes, ref, dev = _pair(case)
+    np.testing.assert_array_equal(dev.u, case["u"])
+    np.testing.assert_array_equal(dev.v, case["v"])
+    np.testing.assert_array_equal(dev.data, ref.data)
+    np.testing.assert_array_equal(dev.to_codes(), codes)
+    np.testing.assert_array_equal(dev.aty_genetic(case["r"]), case["aty"])
+    got_ax = dev.ax_columns(case["support"], case["weights"])
+    if 4 * case["support"].size < case["p"]:
+        # the reference's column sweep (geno_matrix.py:346-348): same operation order
+        np.testing.assert_array_equal(got_ax, case["ax"])
+    else:
+        # the reference switches to its sample-major sweep (:337-345), which sums
+        # the same terms in another order
+        np.testing.assert_allclose(got_ax, case["ax"], rtol=1e-13, atol=1e-14)
+    np.testing.assert_array_equal(dev.decompress(case["support"]), case["decompress"])
+
+
+@pytest.mark.parametrize("name", sorted(golden_io.load("kernels")))
+def test_fast_aty_tolerance(name):
+    # the IHT loop's lookup-table kernel: fp32 tables, fp64 accumulation.
+    # Tolerance 2e-6 of rms(g) -- the sensitivity bound below which supports and
+    # iteration counts are unchanged, 10x under 2e-5.
+    case = golden_io.load("kernels")[name]
+    _, ref, dev = _pair(case)
+    want = case["aty"]
+    got = dev.aty_genetic(case["r"], mode="fast")
+    scale = max(np.sqrt(np.mean(want ** 2)), 1e-300)
+    assert np.max(np.abs(got - want)) <= 2e-6 * scale + 1e-12
+
+
+@pytest.mark.parametrize("n,p,miss", [(1, 1, 0.0), (3, 33, 0.3), (511, 64, 0.0), (513, 65, 0.02),
+                                      (1030, 700, 0.05), (4099, 3000, 0.0), (20000, 257, 0.01)])
+def test_kernels_vs_oracle_shapes(n, p, miss):
+    rng = np.random.default_rng(n * 7919 + p)
+    codes = oracle.random_codes(n, p, seed=n + p, missing_rate=miss)
+    ref = oracle.OraclePacked.from_codes(codes)
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    np.testing.assert_array_equal(dev.u, ref.u)
+    np.testing.assert_array_equal(dev.v, ref.v)
+    r = rng.standard_normal(n) + 3.0  # uncentred on purpose
+    want = ref.aty_genetic(r)
+    np.testing.assert_array_equal(dev.aty_genetic(r), want)
+    fast = dev.aty_genetic(r, mode="fast")
+    scale = max(np.sqrt(np.mean(want ** 2)), 1e-300)
+    assert np.max(np.abs(fast - want)) <= 2e-6 * scale + 1e-12
+    k = min(p, 17)
+    idx = np.sort(rng.choice(p, k, replace=False))
+    w = rng.standard_normal(k)
+    if 4 * k < p:  # the reference's column-sweep branch (geno_matrix.py:346-348)
+        np.testing.assert_array_equal(dev.ax_columns(idx, w), ref.ax_columns(idx, w))
+    else:
+        np.testing.assert_allclose(dev.ax_columns(idx, w), ref.ax_columns(idx, w),
+                                   rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(dev.decompress(idx), ref.decompress(idx))
+
+
+def test_subset_rows_and_masked_stats():
+    rng = np.random.default_rng(5)
+    codes = oracle.random_codes(777, 130, seed=3, missing_rate=0.1)
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    rows = np.sort(rng.choice(777, 500, replace=False))
+    sub = dev.subset_rows(rows)
+    np.testing.assert_array_equal(sub.to_codes(), codes[rows])
+    ref = oracle.OraclePacked.from_codes(codes[rows])
+    np.testing.assert_array_equal(sub.u, ref.u)
+    np.testing.assert_array_equal(sub.v, ref.v)
+    keep = np.zeros(777, np.uint8)
+    keep[rows] = 1
+    u, v = dev.masked_stats(keep)
+    np.testing.assert_array_equal(u, ref.u)
+    np.testing.assert_array_equal(v, ref.v)
+
+
+def test_synth_matches_cpu_twin():
+    gi = _gm()
+    for n, p, miss, j0 in [(1000, 70, 0.0, 0), (517, 45, 0.02, 123)]:
+        dev = gi.PackedGenotypeMatrix.synthetic(n, p, seed=1608, missing_rate=miss, j_base=j0)
+        np.testing.assert_array_equal(dev.data, oracle.synth_bed(1608, n, j0, p, missing=miss))
+
+
+def test_with_stats_shares_bytes():
+    codes = oracle.random_codes(50, 20, seed=9, missing_rate=0.1)
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    u = np.linspace(0, 2, 20)
+    v = np.linspace(0, 1, 20)
+    other = dev.with_stats(u, v)
+    np.testing.assert_array_equal(other.u, u)
+    np.testing.assert_array_equal(other.data, dev.data)
+    ref = oracle.OraclePacked.from_codes(codes).with_stats(u, v)
+    r = np.random.default_rng(1).standard_normal(50)
+    np.testing.assert_array_equal(other.aty_genetic(r), ref.aty_genetic(r))
