@@ -94,18 +94,23 @@ int gi_decompress(gi_matrix *h, const int64_t *idx, int64_t k, double *out_t);
 /* u, v may be NULL to use the handle's own statistics. */
 int gi_dev_ax(gi_matrix *h, const double *u, const double *v, const int64_t *d_idx,
               const double *d_w, int64_t k, double *d_out, int accumulate, void *stream);
-/* g = scale * X^T r with the lookup-table kernel; d_rt is fp32(r - mean) padded
- * to gi_padded_samples(h) entries, d_sum_rt a device scalar (sum of d_rt). */
-int gi_dev_aty_fast(gi_matrix *h, const double *u, const double *v, const float *d_rt,
-                    const double *d_sum_rt, double scale, double *d_out, void *stream);
+/* g = scale * X^T r with the lookup-table kernel.  d_rt = fp32(r - mean) on the
+ * view's rows (zero elsewhere), padded to gi_padded_samples(h) entries, as
+ * written by gi_dev_center; d_scal[1] = mean, d_scal[2] = sum(d_rt).
+ * d_s1cnt: per-SNP (sum of dosages, observed count) over the view's rows
+ * (gi_dev_stats), NULL = all rows of the handle. */
+int gi_dev_aty_fast(gi_matrix *h, const double *u, const double *v, const int32_t *d_s1cnt,
+                    const float *d_rt, const double *d_scal, double scale, double *d_out,
+                    void *stream);
 /* exact kernel: d_rpad fp64 padded to gi_padded_samples(h), d_sum_r device scalar */
 int gi_dev_aty_exact(gi_matrix *h, const double *u, const double *v, const double *d_rpad,
                      const double *d_sum_r, double scale, double *d_out, void *stream);
 int64_t gi_padded_samples(const gi_matrix *h);
 /* masked column statistics into device arrays; d_rowmask has one uint32 per
- * (tile, word) = gi_padded_samples/16 entries, bit 2s set for included sample s */
+ * (tile, word) = gi_padded_samples/16 entries, bit 2s set for included sample s
+ * (NULL = all rows); d_s1cnt (optional) receives int32 (sum, count) pairs */
 int gi_dev_stats(gi_matrix *h, const uint32_t *d_rowmask, double *d_u, double *d_v,
-                 void *stream);
+                 int32_t *d_s1cnt, void *stream);
 
 /* Reduction workspace: d_partials >= gi_red_partials() doubles, d_ticket one
  * zero-initialised uint32 (the kernels leave it zero again). */

@@ -52,10 +52,10 @@ def _declare(lib):
         "gi_ax_cols": ([P, P, P, c_i64, P], c_int),
         "gi_decompress": ([P, P, c_i64, P], c_int),
         "gi_dev_ax": ([P, P, P, P, P, c_i64, P, c_int, P], c_int),
-        "gi_dev_aty_fast": ([P, P, P, P, P, c_dbl, P, P], c_int),
+        "gi_dev_aty_fast": ([P, P, P, P, P, P, c_dbl, P, P], c_int),
         "gi_dev_aty_exact": ([P, P, P, P, P, c_dbl, P, P], c_int),
         "gi_padded_samples": ([P], c_i64),
-        "gi_dev_stats": ([P, P, P, P, P], c_int),
+        "gi_dev_stats": ([P, P, P, P, P, P], c_int),
         "gi_red_partials": ([], c_i64),
         "gi_dev_residual": ([c_i64, P, P, P, c_i64, P, P, c_dbl, P, P, P, P, P], c_int),
         "gi_dev_center": ([c_i64, c_i64, P, P, P, P, P, P, P], c_int),

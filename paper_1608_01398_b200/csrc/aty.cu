@@ -98,7 +98,8 @@ struct FastArgs {
   const float* rt;
   const double* u;
   const double* v;
-  const double* sum_rt;
+  const int32_t* s1cnt;  // per-SNP (sum of dosages, observed count) over the view's rows
+  const double* scal;    // [1] = mean of r used for centring, [2] = sum of rt
   double scale;
   double* out;
   int64_t n_items;
@@ -377,12 +378,17 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         acc[gl * 32 + lane] += add;
       }
     }
-    // epilogue: out_j = scale * v_j * (acc_j - u_j * sum_rt)
-    const double srt = *a.sum_rt;
+    // epilogue: out_j = scale * v_j * (acc_j - u_j * sum_rt + mean * (s1_j - u_j cnt_j));
+    // the last term restores the constant part of r removed by centring (zero
+    // up to rounding when u_j is the mean over the same rows; not for
+    // caller-supplied stats such as with_stats / global-standardised folds)
+    const double mean = a.scal[1], srt = a.scal[2];
     for (uint32_t gl = warp; gl < ng; gl += kWarps) {
       const int64_t j = (g0 + gl) * 32 + lane;
       if (j < m.p) {
-        const double val = a.v[j] * (acc[gl * 32 + lane] - a.u[j] * srt);
+        const double uj = a.u[j];
+        const double off = (double)a.s1cnt[2 * j] - uj * (double)a.s1cnt[2 * j + 1];
+        const double val = a.v[j] * ((acc[gl * 32 + lane] - uj * srt) + mean * off);
         a.out[j] = a.scale * val;
       }
     }
@@ -393,8 +399,9 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
 int g_aty_flags = 0;  // experiment knobs (GI_ATY_FLAGS)
 
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
-                    const double* u, const double* v, const double* d_sum_rt, double scale,
-                    double* out, int num_sms, cudaStream_t s) {
+                    const double* u, const double* v, const int32_t* s1cnt,
+                    const double* d_scal, double scale, double* out, int num_sms,
+                    cudaStream_t s) {
   if (m.p == 0) return 0;
   static bool configured = false;
   if (!configured) {
@@ -410,7 +417,8 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
   a.rt = rt;
   a.u = u;
   a.v = v;
-  a.sum_rt = d_sum_rt;
+  a.s1cnt = s1cnt;
+  a.scal = d_scal;
   a.scale = scale;
   a.out = out;
   a.flags = g_aty_flags;

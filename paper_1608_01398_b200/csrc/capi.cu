@@ -100,6 +100,7 @@ struct gi_matrix {
   std::shared_ptr<DevMem> x;         // swizzled tiles (shared by with_stats copies)
   std::shared_ptr<DevMem> miss_cnt;  // int32[p]
   std::shared_ptr<DevMem> gmiss;     // uint8[G]
+  std::shared_ptr<DevMem> s1cnt;     // int32[2p]: sum of dosages, observed count (all rows)
   std::shared_ptr<DevMem> u, v;      // fp64[p], owned per handle
   cudaStream_t stream = nullptr;
   std::mutex mu;
@@ -147,13 +148,14 @@ static int matrix_shell(int64_t n, int64_t p, int device, gi_matrix** out,
   TRY(alloc(h->v, sizeof(double) * p, device, true));
   TRY(alloc(h->miss_cnt, sizeof(int32_t) * p, device, true));
   TRY(alloc(h->gmiss, (size_t)h->G, device, true));
+  TRY(alloc(h->s1cnt, sizeof(int32_t) * 2 * p, device, true));
   return 0;
 }
 
 static int finish_stats(gi_matrix* h) {
   gi::MatrixDesc d = h->desc();
   TRY(gi::launch_stats(d, nullptr, h->du(), h->dv(), static_cast<int32_t*>(h->miss_cnt->ptr),
-                       h->stream));
+                       static_cast<int32_t*>(h->s1cnt->ptr), h->stream));
   TRY(gi::launch_group_flags(d, static_cast<int32_t*>(h->miss_cnt->ptr),
                              static_cast<uint8_t*>(h->gmiss->ptr), h->stream));
   GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -257,6 +259,7 @@ int gi_matrix_with_stats(const gi_matrix* src, const double* u, const double* v,
   h->x = src->x;
   h->miss_cnt = src->miss_cnt;
   h->gmiss = src->gmiss;
+  h->s1cnt = src->s1cnt;
   DeviceGuard g(h->device);
   GI_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   TRY(alloc(h->u, sizeof(double) * h->p, h->device, false));
@@ -368,7 +371,8 @@ int gi_matrix_masked_stats(const gi_matrix* hc, const uint8_t* keep, double* u, 
   GI_CUDA_TRY(cudaMemcpyAsync(h->s_a.mem->ptr, mask.data(), mask.size() * 4,
                               cudaMemcpyHostToDevice, h->stream));
   double* du = h->s_b.as<double>();
-  TRY(gi::launch_stats(h->desc(), h->s_a.as<uint32_t>(), du, du + h->p, nullptr, h->stream));
+  TRY(gi::launch_stats(h->desc(), h->s_a.as<uint32_t>(), du, du + h->p, nullptr, nullptr,
+                       h->stream));
   GI_CUDA_TRY(cudaMemcpyAsync(u, du, sizeof(double) * h->p, cudaMemcpyDeviceToHost, h->stream));
   GI_CUDA_TRY(cudaMemcpyAsync(v, du + h->p, sizeof(double) * h->p, cudaMemcpyDeviceToHost,
                               h->stream));
@@ -405,7 +409,8 @@ int gi_aty(gi_matrix* h, const double* r, double sum_r, double* out, int mode) {
                             dr, scal, partials, ticket, h->stream));
     TRY(gi::launch_center(h->n, npad, dr, nullptr, scal, drt, partials, ticket, h->stream));
     TRY(gi::launch_aty_fast(h->desc(), static_cast<const uint8_t*>(h->gmiss->ptr), drt, h->du(),
-                            h->dv(), scal + 2, 1.0, h->s_b.as<double>(), h->sms, h->stream));
+                            h->dv(), static_cast<const int32_t*>(h->s1cnt->ptr), scal, 1.0,
+                            h->s_b.as<double>(), h->sms, h->stream));
   }
   GI_CUDA_TRY(cudaMemcpyAsync(out, h->s_b.mem->ptr, sizeof(double) * h->p,
                               cudaMemcpyDeviceToHost, h->stream));
@@ -464,12 +469,14 @@ int gi_dev_ax(gi_matrix* h, const double* u, const double* v, const int64_t* d_i
                        accumulate, STREAM(stream));
 }
 
-int gi_dev_aty_fast(gi_matrix* h, const double* u, const double* v, const float* d_rt,
-                    const double* d_sum_rt, double scale, double* d_out, void* stream) {
-  CHECK_ARG(h && d_rt && d_sum_rt && d_out, "NULL argument");
+int gi_dev_aty_fast(gi_matrix* h, const double* u, const double* v, const int32_t* d_s1cnt,
+                    const float* d_rt, const double* d_scal, double scale, double* d_out,
+                    void* stream) {
+  CHECK_ARG(h && d_rt && d_scal && d_out, "NULL argument");
   return gi::launch_aty_fast(h->desc(), static_cast<const uint8_t*>(h->gmiss->ptr), d_rt,
-                             u ? u : h->du(), v ? v : h->dv(), d_sum_rt, scale, d_out, h->sms,
-                             STREAM(stream));
+                             u ? u : h->du(), v ? v : h->dv(),
+                             d_s1cnt ? d_s1cnt : static_cast<const int32_t*>(h->s1cnt->ptr),
+                             d_scal, scale, d_out, h->sms, STREAM(stream));
 }
 
 int gi_dev_aty_exact(gi_matrix* h, const double* u, const double* v, const double* d_rpad,
@@ -480,9 +487,9 @@ int gi_dev_aty_exact(gi_matrix* h, const double* u, const double* v, const doubl
 }
 
 int gi_dev_stats(gi_matrix* h, const uint32_t* d_rowmask, double* d_u, double* d_v,
-                 void* stream) {
+                 int32_t* d_s1cnt, void* stream) {
   CHECK_ARG(h && d_u && d_v, "NULL argument");
-  return gi::launch_stats(h->desc(), d_rowmask, d_u, d_v, nullptr, STREAM(stream));
+  return gi::launch_stats(h->desc(), d_rowmask, d_u, d_v, nullptr, d_s1cnt, STREAM(stream));
 }
 
 int64_t gi_red_partials(void) { return 8 * 296; }

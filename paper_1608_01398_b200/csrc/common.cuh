@@ -108,12 +108,13 @@ int launch_synth(const MatrixDesc& m, uint8_t* x, uint64_t seed, int64_t j_base,
 int launch_subset_rows(const MatrixDesc& src, const MatrixDesc& dst, uint8_t* x,
                        const int64_t* d_rows, cudaStream_t s);
 int launch_stats(const MatrixDesc& m, const uint32_t* d_rowmask, double* u, double* v,
-                 int32_t* d_missing_cnt, cudaStream_t s);
+                 int32_t* d_missing_cnt, int32_t* d_s1cnt, cudaStream_t s);
 int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_t* flags,
                        cudaStream_t s);
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
-                    const double* u, const double* v, const double* d_sum_rt, double scale,
-                    double* out, int num_sms, cudaStream_t s);
+                    const double* u, const double* v, const int32_t* s1cnt,
+                    const double* d_scal, double scale, double* out, int num_sms,
+                    cudaStream_t s);
 int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u,
                      const double* v, const double* d_sum_r, double scale, double* out,
                      cudaStream_t s);

@@ -142,7 +142,7 @@ int launch_synth(const MatrixDesc& m, uint8_t* x, uint64_t seed, int64_t j_base,
 // 16w + s of the tile is included (cross-validation training rows).
 __global__ void stats_kernel(MatrixDesc m, const uint32_t* __restrict__ rowmask,
                              double* __restrict__ u, double* __restrict__ v,
-                             int32_t* __restrict__ missing_cnt) {
+                             int32_t* __restrict__ missing_cnt, int32_t* __restrict__ s1cnt) {
   const int lane = threadIdx.x & 31;
   const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (g >= m.G) return;
@@ -181,14 +181,19 @@ __global__ void stats_kernel(MatrixDesc m, const uint32_t* __restrict__ rowmask,
   }
   v[j] = vj;
   if (missing_cnt) missing_cnt[j] = miss;
+  if (s1cnt) {
+    s1cnt[2 * j] = s1;
+    s1cnt[2 * j + 1] = cnt;
+  }
 }
 
 int launch_stats(const MatrixDesc& m, const uint32_t* d_rowmask, double* u, double* v,
-                 int32_t* d_missing_cnt, cudaStream_t s) {
+                 int32_t* d_missing_cnt, int32_t* d_s1cnt, cudaStream_t s) {
   if (m.p == 0) return 0;
   const int threads = 256;
   const int64_t blocks = (m.G * 32 + threads - 1) / threads;
-  stats_kernel<<<(unsigned)blocks, threads, 0, s>>>(m, d_rowmask, u, v, d_missing_cnt);
+  stats_kernel<<<(unsigned)blocks, threads, 0, s>>>(m, d_rowmask, u, v, d_missing_cnt,
+                                                     d_s1cnt);
   GI_LAUNCH_CHECK();
   return 0;
 }

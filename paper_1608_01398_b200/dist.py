@@ -110,3 +110,44 @@ def merge_topk(keys: np.ndarray, idx: np.ndarray, vals: np.ndarray, k: int):
     take = order[:k]
     sel = np.argsort(idx[take], kind="stable")
     return idx[take][sel].astype(np.int64), vals[take][sel]
+
+
+class ShardedGenotypes:
+    """This rank's SNP block of a matrix sharded over ``comm.world`` GPUs.
+
+    Behaves like a packed matrix of the GLOBAL shape for the solver (global
+    SNP indices everywhere); the fit engine runs on the local block and joins
+    the shards through ``comm``."""
+
+    def __init__(self, local, j_base: int, p_global: int, comm):
+        self.local = local
+        self.j_base = int(j_base)
+        self.p = int(p_global)
+        self.n = local.n
+        self.device = local.device
+        self.comm = comm
+
+    @classmethod
+    def synthetic(cls, n: int, p: int, seed: int, comm, device: int, maf_range=(0.05, 0.5),
+                  missing_rate: float = 0.0):
+        from .geno_matrix import PackedGenotypeMatrix
+
+        j0, j1 = shard_range(p, comm.world, comm.rank)
+        local = PackedGenotypeMatrix.synthetic(n, j1 - j0, seed, maf_range=maf_range,
+                                               missing_rate=missing_rate, device=device,
+                                               j_base=j0)
+        return cls(local, j0, p, comm)
+
+    def engine_genotypes(self):
+        from .engine import Genotypes
+
+        return Genotypes(self.local, j_base=self.j_base, p_global=self.p, comm=self.comm)
+
+    def ax_columns(self, idx, w) -> np.ndarray:
+        idx = np.asarray(idx, dtype=np.int64)
+        w = np.asarray(w, dtype=np.float64)
+        if idx.size and (idx.min() < 0 or idx.max() >= self.p):
+            raise IndexError("variant index out of range")
+        sel = (idx >= self.j_base) & (idx < self.j_base + self.local.p)
+        part = self.local.ax_columns(idx[sel] - self.j_base, w[sel])
+        return self.comm.allreduce_sum_host(part)

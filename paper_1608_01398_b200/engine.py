@@ -32,6 +32,10 @@ def _torch():
     return torch
 
 
+def torch_event():
+    return _torch().cuda.Event(enable_timing=True)
+
+
 class Genotypes:
     """What the engine needs to know about the genotype operand of a view.
 
@@ -123,6 +127,20 @@ class DeviceEngine:
         self.u_ptr = None if geno.u is None else geno.u.data_ptr()
         self.v_ptr = None if geno.v is None else geno.v.data_ptr()
         self.kernel_launches = 0
+        self.aty_events = None  # list of (start, end) CUDA events when profiling
+        # per-SNP (sum of dosages, observed count) over the view's rows: the fast
+        # X^T r kernel restores the mean of r removed by centring with them
+        self.s1cnt = None
+        if geno.rows is not None:
+            mask = np.zeros(self.n_pad // 16, np.uint32)
+            np.bitwise_or.at(mask, geno.rows >> 4, (1 << (2 * (geno.rows & 15))).astype(np.uint32))
+            d_mask = torch.as_tensor(mask.view(np.int32)).to(dev)
+            scratch = torch.zeros(2 * max(self.p, 1), dtype=f64, device=dev)
+            self.s1cnt = torch.zeros(2 * max(self.p, 1), dtype=torch.int32, device=dev)
+            P = _native.ptr
+            check(lib().gi_dev_stats(self.h, P(d_mask), P(scratch), P(scratch) + 8 * self.p,
+                                     P(self.s1cnt), self.s))
+            self.kernel_launches += 1
 
     # ------------------------------------------------------------- helpers
     def _ensure_kbuf(self, k):
@@ -132,23 +150,55 @@ class DeviceEngine:
         k = max(k, 2 * self._kbuf)
         self.d_idx = torch.zeros(k, dtype=torch.int64, device=self.dev)
         self.d_w = torch.zeros(k, dtype=torch.float64, device=self.dev)
-        self.h_idx = torch.zeros(k, dtype=torch.int64).pin_memory()
-        self.h_w = torch.zeros(k, dtype=torch.float64).pin_memory()
         self._kbuf = k
+        self._grow_pool(8 * k)
+
+    def _grow_pool(self, words):
+        """Pinned staging for H2D copies.  Every copy gets its own region (bump
+        allocation) and regions are recycled only after a stream sync, so the host
+        never overwrites bytes an enqueued copy has not read yet."""
+        if getattr(self, "_pool_words", 0) >= words:
+            return
+        if getattr(self, "_pool_used", 0):
+            self._sync()
+        self._pool = self.torch.zeros(words, dtype=self.torch.float64).pin_memory()
+        self._pool_np = self._pool.numpy()
+        self._pool_words = words
+        self._pool_used = 0
+
+    def _stage(self, values: np.ndarray, dtype) -> "object":
+        """Copy ``values`` into a fresh pinned region; returns the pinned tensor view."""
+        k = int(values.size)
+        if self._pool_used + k > self._pool_words:
+            self._sync()
+            self._grow_pool(max(self._pool_words, 2 * k))
+        lo = self._pool_used
+        self._pool_used += k
+        region = self._pool[lo:lo + k]
+        if dtype == "i64":
+            region = region.view(self.torch.int64)
+            region.numpy()[:] = values
+        else:
+            region.numpy()[:] = values
+        return region
 
     def _upload_sparse(self, idx_local: np.ndarray, w: np.ndarray) -> int:
         k = int(idx_local.size)
         if k == 0:
             return 0
         self._ensure_kbuf(k)
-        self.h_idx.numpy()[:k] = idx_local
-        self.h_w.numpy()[:k] = w
-        self.d_idx[:k].copy_(self.h_idx[:k], non_blocking=True)
-        self.d_w[:k].copy_(self.h_w[:k], non_blocking=True)
+        self.d_idx[:k].copy_(self._stage(np.asarray(idx_local, np.int64), "i64"),
+                             non_blocking=True)
+        self.d_w[:k].copy_(self._stage(np.asarray(w, np.float64), "f64"), non_blocking=True)
         return k
+
+    def _upload_cov(self, values) -> None:
+        self.cvec[: self.c].copy_(self._stage(np.asarray(values, np.float64), "f64"),
+                                  non_blocking=True)
 
     def _sync(self):
         self.stream.synchronize()
+        self._pool_used = 0
 
     def local_part(self, idx_global: np.ndarray, w: np.ndarray):
         """Entries of a global sparse vector owned by this shard (local indices)."""
@@ -170,6 +220,9 @@ class DeviceEngine:
             self.comm.allreduce_sum_(out)
 
     # --------------------------------------------------------------- phases
+    def reset_beta(self):
+        self.beta.zero_()
+
     def set_beta(self, old_idx, new_idx, new_w):
         """Dense device beta: zero the old support, write the new one."""
         P = _native.ptr
@@ -194,8 +247,7 @@ class DeviceEngine:
         if has_fit:
             self._ax_into(self.fit, support, weights)
         if self.c:
-            self.h_out.numpy()[: self.c] = bcov
-            self.cvec[: self.c].copy_(self.h_out[: self.c], non_blocking=True)
+            self._upload_cov(bcov)
         cptr = P(self.cvec)
         gcov_ptr = cptr + 8 * self.c if self.c else None
         check(L.gi_dev_residual(self.n, P(self.y), P(self.fit) if has_fit else None,
@@ -207,8 +259,15 @@ class DeviceEngine:
                               P(self.keep) if self.keep is not None else None, P(self.scal),
                               P(self.rt), P(self.partials), P(self.ticket), self.s))
         if self.p:
-            check(L.gi_dev_aty_fast(self.h, self.u_ptr, self.v_ptr, P(self.rt),
-                                    P(self.scal) + 16, -1.0, P(self.g), self.s))
+            ev = None
+            if self.aty_events is not None:
+                ev = (torch_event(), torch_event())
+                ev[0].record(self.stream)
+            check(L.gi_dev_aty_fast(self.h, self.u_ptr, self.v_ptr, P(self.s1cnt), P(self.rt),
+                                    P(self.scal), -1.0, P(self.g), self.s))
+            if ev is not None:
+                ev[1].record(self.stream)
+                self.aty_events.append(ev)
             check(L.gi_dev_maxabs(self.p, P(self.g), P(self.scal), 3, P(self.partials),
                                   P(self.ticket), self.s))
         if self.c:
@@ -255,8 +314,7 @@ class DeviceEngine:
         L = lib()
         self._ax_into(self.img, idx, w)
         if wcov is not None and self.c:
-            self.h_out.numpy()[: self.c] = wcov
-            self.cvec[: self.c].copy_(self.h_out[: self.c], non_blocking=True)
+            self._upload_cov(wcov)
             check(L.gi_dev_add_cov(self.n, P(self.C), self.c, P(self.cvec), P(self.img), self.s))
             self.kernel_launches += 1
         if self.keep is not None:
