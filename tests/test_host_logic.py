@@ -1,0 +1,118 @@
+"""Host-side logic of the drop-in that runs without a GPU: projection and
+top-k rules, fold bookkeeping, configuration validation, codes packing and
+the per-shard top-k merge.  Cases mirror the reference's own tests
+(pkg/tests/test_iht.py:33-69, test_model_select.py:28-61, test_plink_io.py:16-24)."""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1608_01398_b200 as gi
+from paper_1608_01398_b200.dist import merge_topk, shard_range
+
+
+def test_project_examples():
+    m = gi.project_sparse(np.array([3.0, -1.0, 0.5, 2.0]), 2)
+    np.testing.assert_array_equal(m.dense_genetic(), [3.0, 0.0, 0.0, 2.0])
+    m = gi.project_sparse(np.array([2.0, -2.0, 0.0]), 1)  # tie -> lower index
+    np.testing.assert_array_equal(m.dense_genetic(), [2.0, 0.0, 0.0])
+    m = gi.project_sparse(np.array([1.0, -1.0, 1.0]), 3)
+    np.testing.assert_array_equal(m.dense_genetic(), [1.0, -1.0, 1.0])
+
+
+def test_hard_threshold_matches_oracle(rng):
+    for _ in range(300):
+        p = int(rng.integers(1, 30))
+        k = int(rng.integers(0, 8))
+        vec = np.round(rng.standard_normal(p), int(rng.integers(0, 3)))  # rounding makes ties
+        np.testing.assert_array_equal(gi.hard_threshold(vec, k), oracle.threshold_k(vec, k))
+
+
+def test_top_k_large(rng):
+    vec = rng.standard_normal(200_000)
+    idx = gi.top_k_indices(np.abs(vec), 10)
+    assert set(idx) == set(np.argsort(-np.abs(vec))[:10])
+
+
+def test_merge_topk_matches_global_rule(rng):
+    # per-shard local top-k lists merged == global top-k with ties to lower index
+    for _ in range(200):
+        p = int(rng.integers(1, 60))
+        k = int(rng.integers(1, 10))
+        world = int(rng.integers(1, 5))
+        vals = np.round(rng.standard_normal(p), 1)
+        vals[rng.random(p) < 0.2] = 0.0
+        keys_all = np.abs(vals).view(np.uint64) + np.uint64(1)
+        ks, ii, vv = [], [], []
+        for r in range(world):
+            j0, j1 = shard_range(p, world, r)
+            loc = np.arange(j0, j1)
+            order = np.lexsort((loc, ~keys_all[loc]))[:k]
+            ks.append(keys_all[loc][order])
+            ii.append(loc[order])
+            vv.append(vals[loc][order])
+        idx, got = merge_topk(np.concatenate(ks), np.concatenate(ii), np.concatenate(vv), k)
+        want_idx = oracle.top_k(np.abs(vals), k)
+        np.testing.assert_array_equal(idx, want_idx)
+        np.testing.assert_array_equal(got, vals[want_idx])
+
+
+def test_shard_range_partitions():
+    for p, world in itertools.product([0, 1, 7, 100, 1001], [1, 2, 3, 8]):
+        spans = [shard_range(p, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == p
+        for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+            assert a1 == b0
+        sizes = [b - a for a, b in spans]
+        assert max(sizes) - min(sizes) <= 1
+
+
+def test_folds_match_reference_rule():
+    for n, q, seed in [(10, 5, 0), (7, 3, 0), (40, 4, 9), (2000, 5, 2016)]:
+        np.testing.assert_array_equal(gi.make_folds(n, q, seed), oracle.folds(n, q, seed))
+    assert np.bincount(gi.make_folds(10, 5, 0)).tolist() == [2] * 5
+    with pytest.raises(ValueError):
+        gi.make_folds(5, 1, 0)
+    with pytest.raises(ValueError):
+        gi.make_folds(5, 6, 0)
+
+
+def test_plan_and_select():
+    with pytest.raises(ValueError):
+        gi.CvPlan.build(20, 4, [3, 2, 5], seed=0)
+    with pytest.raises(ValueError):
+        gi.CvPlan.build(20, 4, [0, 1], seed=0)
+    path = np.array([2, 4, 6])
+    assert gi.select_k(path, np.array([0.5, 0.25, 0.25])) == 4
+    assert gi.select_k(path, np.array([0.25, 0.25, 0.25])) == 2
+
+
+def test_config_validation():
+    for bad in (dict(k=-1), dict(k=1, tol=0.0), dict(k=1, c_omega=1.0), dict(k=1, max_iter=0),
+                dict(k=1, max_backtracks=-1)):
+        with pytest.raises(ValueError):
+            gi.IhtConfig(**bad)
+
+
+def test_sparse_model_rules():
+    m = gi.SparseModel.from_parts([5, 1, 3], [0.0, 2.0, -1.0], np.zeros(1), k=3, p=10)
+    np.testing.assert_array_equal(m.support, [1, 3])
+    with pytest.raises(ValueError):
+        gi.SparseModel(support=np.array([3, 1]), weights=np.ones(2), covar=np.zeros(0), k=2, p=5)
+
+
+def test_pack_codes_kat():
+    # the byte 0b11100100 holds codes 0, 1, 2, 3 from the least significant pair
+    assert gi.pack_codes(np.array([[0, 1, 2, 3]], np.uint8))[0, 0] == 0b11100100
+    codes = np.random.default_rng(3).integers(0, 4, size=(9, 13)).astype(np.uint8)
+    np.testing.assert_array_equal(gi.unpack_codes(gi.pack_codes(codes), 13), codes)
+    np.testing.assert_array_equal(gi.pack_codes(codes), oracle.pack_codes(codes))
+
+
+def test_covariate_block():
+    raw = np.random.default_rng(2).standard_normal((10, 2)) * 5 + 2
+    block = gi.CovariateBlock.build(raw, add_intercept=True)
+    np.testing.assert_array_equal(block.values[:, 0], np.ones(10))
+    assert block.labels[0] == "intercept"
+    np.testing.assert_allclose(block.values[:, 1:].mean(axis=0), 0.0, atol=1e-12)
