@@ -146,6 +146,8 @@ class PackedGenotypeMatrix:
         return cls(h, n, p, device)
 
     # ------------------------------------------------------------ attributes
+    is_cuda = True  # lets a patched genoiht.fit / cv_iht dispatch to the device loop
+
     def _fetch_stats(self):
         with self._lock:
             if self._u is None:
