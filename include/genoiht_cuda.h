@@ -155,6 +155,52 @@ int gi_dev_scatter(int64_t k, const int64_t *d_idx, const double *d_val, double 
 int gi_dev_gather(int64_t k, const int64_t *d_idx, const double *d_src, double *d_dst,
                   void *stream);
 
+/* ------------------------------------------------------ native solver loop */
+/* IhtConfig (iht.py:120-140) */
+typedef struct {
+  int64_t k;
+  int64_t max_iter;
+  double tol;
+  double c_omega;
+  int64_t max_backtracks;
+  int64_t flags;  /* bit 0: time every X^T r launch with CUDA events (aty_ms_total) */
+} gi_fit_config;
+
+/* FitResult (iht.py:172-180); caller-allocated arrays, capacities in *_cap */
+typedef struct {
+  int64_t *support;      /* out: sorted support (nonzero weights only) */
+  double *weights;       /* out: matching weights */
+  int64_t support_cap;   /* in: >= max(k, warm_k) */
+  int64_t nnz;           /* out */
+  double *covar;         /* out: c covariate coefficients */
+  double *loss_trace;    /* out: loss after initial state and each accepted step */
+  int64_t trace_cap;     /* in: >= max_iter + 1 */
+  int64_t trace_len;     /* out */
+  int64_t iterations;    /* out */
+  int64_t backtracks;    /* out: total step halvings */
+  int64_t kernel_launches; /* out */
+  double aty_ms_total;   /* out: summed X^T r kernel time (flags bit 0) */
+  int64_t aty_launches;  /* out: X^T r launches */
+  int reason;            /* out: 0 converged, 1 max-iter, 2 step-size collapse */
+} gi_fit_result;
+
+/* Replaces genoiht.fit (iht.py:326-354) on one GPU: the complete IHT loop with
+ * device kernels, one host sync per phase.  y (n) and C (row-major n x c,
+ * c <= 8) are host arrays over the handle's n samples; keep (n, optional)
+ * restricts the fit to rows with keep != 0 (cross-validation training rows:
+ * other rows' residuals are pinned to 0); u, v (p, optional) override the
+ * handle's stats; warm_idx/warm_w (warm_k, sorted, may be NULL) seed the
+ * support; bcov0 (c) is the initial covariate block (least squares on the
+ * caller side, as in initial_state iht.py:207-208).  y == NULL reuses the y, C,
+ * keep and stats left resident on the device by the previous gi_fit call on
+ * this handle (benchmarks).  Returns 0, -1 (CUDA /
+ * argument error), -2 "gradient vanishes ..." (ValueError, iht.py:237),
+ * -3 "degenerate active set ..." (ValueError, iht.py:243) or -4 "loss diverged
+ * ..." (FloatingPointError, iht.py:348). */
+int gi_fit(gi_matrix *h, const double *y, const double *C, int64_t c, const uint8_t *keep,
+           const double *u, const double *v, const gi_fit_config *cfg, const int64_t *warm_idx,
+           const double *warm_w, int64_t warm_k, const double *bcov0, gi_fit_result *res);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,6 +29,23 @@ class NativeError(RuntimeError):
     """A CUDA-side failure reported through gi_last_error()."""
 
 
+class FitConfig(ctypes.Structure):
+    """gi_fit_config (IhtConfig, iht.py:120-140)."""
+
+    _fields_ = [("k", c_i64), ("max_iter", c_i64), ("tol", c_dbl), ("c_omega", c_dbl),
+                ("max_backtracks", c_i64), ("flags", c_i64)]
+
+
+class FitOut(ctypes.Structure):
+    """gi_fit_result (FitResult, iht.py:172-180)."""
+
+    _fields_ = [("support", c_vp), ("weights", c_vp), ("support_cap", c_i64), ("nnz", c_i64),
+                ("covar", c_vp), ("loss_trace", c_vp), ("trace_cap", c_i64),
+                ("trace_len", c_i64), ("iterations", c_i64), ("backtracks", c_i64),
+                ("kernel_launches", c_i64), ("aty_ms_total", c_dbl), ("aty_launches", c_i64),
+                ("reason", c_int)]
+
+
 def _declare(lib):
     P = c_vp
     sig = {
@@ -67,6 +84,8 @@ def _declare(lib):
         "gi_dev_topk": ([c_i64, c_i64, c_int, P, P, c_dbl, c_i64, P, P, P, P, P, P, P, P], c_int),
         "gi_dev_scatter": ([c_i64, P, P, P, P], c_int),
         "gi_dev_gather": ([c_i64, P, P, P, P], c_int),
+        "gi_fit": ([P, P, P, c_i64, P, P, P, ctypes.POINTER(FitConfig), P, P, c_i64, P,
+                    ctypes.POINTER(FitOut)], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

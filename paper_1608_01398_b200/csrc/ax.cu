@@ -46,12 +46,27 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
     for (int s = 0; s < 16; ++s) acc[s] = (accumulate && s < cnt) ? out[i0 + s] : 0.0;
     const int64_t tile = wg >> 5;
     const int wp = (int)(wg & 31);
-    for (int t = 0; t < k; ++t) {
-      if (!live[t]) continue;
-      const uint32_t word =
-          *reinterpret_cast<const uint32_t*>(m.x + word_offset(tile, cols[t], wp, m.G));
+    // columns in batches of 8: issue the 8 independent word loads first, then
+    // accumulate in the caller's column order (same per-sample add sequence)
+    for (int t0 = 0; t0 < k; t0 += 8) {
+      uint32_t words[8];
 #pragma unroll
-      for (int s = 0; s < 16; ++s) acc[s] = __dadd_rn(acc[s], terms[t][(word >> (2 * s)) & 3u]);
+      for (int b = 0; b < 8; ++b) {
+        const int t = t0 + b;
+        words[b] = (t < k && live[t])
+                       ? __ldg(reinterpret_cast<const uint32_t*>(
+                             m.x + word_offset(tile, cols[t], wp, m.G)))
+                       : 0u;
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int t = t0 + b;
+        if (t < k && live[t]) {
+#pragma unroll
+          for (int s = 0; s < 16; ++s)
+            acc[s] = __dadd_rn(acc[s], terms[t][(words[b] >> (2 * s)) & 3u]);
+        }
+      }
     }
 #pragma unroll
     for (int s = 0; s < 16; ++s)

@@ -1,0 +1,546 @@
+// Native single-GPU IHT loop: gi_fit (include/genoiht_cuda.h).
+//
+// The control flow is the reference solver's, step for step:
+//   fit            iht.py:326-354     initial state, loop, trace, reasons
+//   _refresh_state iht.py:183-191     r = y - X_S b - C b_cov, loss, g = -X^T r
+//   iht_step       iht.py:253-323     fixed points, restriction, mu, backtracking
+//   _step_restriction / _normalized_step iht.py:218-244
+// and the same as paper_1608_01398_b200/iht.py (which drives the multi-GPU
+// case through the same kernels).  Every O(n), O(p) and O(n p) operation is a
+// kernel on the matrix's device; the host keeps the O(k) support bookkeeping
+// and recomputes the candidate step with the reference's float operations.
+// One host sync per phase (refresh, image, top-k).
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "../../include/genoiht_cuda.h"
+#include "handle.cuh"
+
+namespace {
+
+struct FitWs {
+  int device = 0;
+  int64_t n = 0, p = 0, npad = 0, c = 0, kcap = 0, slots = 0;
+  cudaStream_t stream = nullptr;
+  // device
+  double *y = nullptr, *C = nullptr, *r = nullptr, *fitb = nullptr, *img = nullptr;
+  double *g = nullptr, *beta = nullptr, *cvec = nullptr, *scal = nullptr, *partials = nullptr;
+  double *u = nullptr, *v = nullptr;
+  float* rt = nullptr;
+  uint8_t* keep = nullptr;
+  int32_t* s1cnt = nullptr;
+  uint32_t *ticket = nullptr, *rowmask = nullptr;
+  uint64_t *ckey = nullptr, *okey = nullptr;
+  int64_t *cidx = nullptr, *oidx = nullptr, *ocnt = nullptr, *didx = nullptr;
+  double *cval = nullptr, *oval = nullptr, *dw = nullptr;
+  // pinned host staging
+  double* hin = nullptr;   // uploads: idx | w | cov (kcap + kcap + 8)
+  double* hout = nullptr;  // downloads
+  std::vector<void*> dev_allocs;
+  bool primed = false, masked = false;
+  double n_eff = 0.0;
+
+  ~FitWs() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* ptr : dev_allocs) cudaFree(ptr);
+    if (hin) cudaFreeHost(hin);
+    if (hout) cudaFreeHost(hout);
+    if (stream) cudaStreamDestroy(stream);
+    cudaSetDevice(prev);
+  }
+
+  template <typename T>
+  int dalloc(T*& out, int64_t count) {
+    void* ptr = nullptr;
+    GI_CUDA_TRY(cudaMalloc(&ptr, sizeof(T) * (size_t)std::max<int64_t>(count, 1)));
+    dev_allocs.push_back(ptr);
+    out = static_cast<T*>(ptr);
+    return 0;
+  }
+};
+
+int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) {
+  auto ws = std::make_shared<FitWs>();
+  ws->device = h->device;
+  ws->n = h->n;
+  ws->p = h->p;
+  ws->npad = h->T * GI_TILE_SAMPLES;
+  ws->c = c;
+  ws->kcap = kcap;
+  ws->slots = gi::topk_blocks(std::max<int64_t>(h->p, 1)) * kcap;
+  GI_CUDA_TRY(cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking));
+  const int64_t n = h->n, p = std::max<int64_t>(h->p, 1);
+  TRY(ws->dalloc(ws->y, n));
+  TRY(ws->dalloc(ws->C, n * std::max<int64_t>(c, 1)));
+  TRY(ws->dalloc(ws->r, n));
+  TRY(ws->dalloc(ws->fitb, n));
+  TRY(ws->dalloc(ws->img, n));
+  TRY(ws->dalloc(ws->g, p));
+  TRY(ws->dalloc(ws->beta, p));
+  TRY(ws->dalloc(ws->cvec, 2 * std::max<int64_t>(c, 1)));
+  TRY(ws->dalloc(ws->scal, 8));
+  TRY(ws->dalloc(ws->partials, 8 * 296));
+  TRY(ws->dalloc(ws->u, p));
+  TRY(ws->dalloc(ws->v, p));
+  TRY(ws->dalloc(ws->rt, ws->npad));
+  TRY(ws->dalloc(ws->keep, n));
+  TRY(ws->dalloc(ws->s1cnt, 2 * p));
+  TRY(ws->dalloc(ws->ticket, 1));
+  TRY(ws->dalloc(ws->rowmask, ws->npad / 16));
+  TRY(ws->dalloc(ws->ckey, ws->slots));
+  TRY(ws->dalloc(ws->cidx, ws->slots));
+  TRY(ws->dalloc(ws->cval, ws->slots));
+  TRY(ws->dalloc(ws->okey, kcap));
+  TRY(ws->dalloc(ws->oidx, kcap));
+  TRY(ws->dalloc(ws->oval, kcap));
+  TRY(ws->dalloc(ws->ocnt, 1));
+  TRY(ws->dalloc(ws->didx, 2 * kcap + 16));
+  TRY(ws->dalloc(ws->dw, 2 * kcap + 16));
+  GI_CUDA_TRY(cudaMemsetAsync(ws->ticket, 0, sizeof(uint32_t), ws->stream));
+  GI_CUDA_TRY(cudaMallocHost(&ws->hin, sizeof(double) * (size_t)(4 * kcap + 64 + 2 * c)));
+  GI_CUDA_TRY(cudaMallocHost(&ws->hout, sizeof(double) * (size_t)(8 + 2 * c + 4 * kcap + 64)));
+  out = ws;
+  return 0;
+}
+
+struct Pair {
+  int64_t idx;
+  double val;
+};
+
+class NativeFit {
+ public:
+  NativeFit(gi_matrix* h, FitWs* ws, const gi_fit_config* cfg, bool masked, double n_eff)
+      : h_(h), ws_(ws), cfg_(*cfg), masked_(masked), n_eff_(n_eff) {}
+
+  int launches = 0;
+  int aty_launches = 0;
+  double aty_ms = 0.0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  // upload a sparse vector (idx, w) into didx/dw
+  int upload_sparse(const std::vector<int64_t>& idx, const std::vector<double>& w) {
+    const int64_t k = (int64_t)idx.size();
+    if (k == 0) return 0;
+    int64_t* hi = reinterpret_cast<int64_t*>(ws_->hin);
+    double* hw = ws_->hin + ws_->kcap * 2 + 16;
+    memcpy(hi, idx.data(), sizeof(int64_t) * k);
+    memcpy(hw, w.data(), sizeof(double) * k);
+    GI_CUDA_TRY(cudaMemcpyAsync(ws_->didx, hi, sizeof(int64_t) * k, cudaMemcpyHostToDevice,
+                                ws_->stream));
+    GI_CUDA_TRY(cudaMemcpyAsync(ws_->dw, hw, sizeof(double) * k, cudaMemcpyHostToDevice,
+                                ws_->stream));
+    return 0;
+  }
+
+  int upload_cov(const std::vector<double>& cv) {
+    if (ws_->c == 0) return 0;
+    double* hc = ws_->hin + 4 * ws_->kcap + 32;
+    memcpy(hc, cv.data(), sizeof(double) * ws_->c);
+    GI_CUDA_TRY(cudaMemcpyAsync(ws_->cvec, hc, sizeof(double) * ws_->c, cudaMemcpyHostToDevice,
+                                ws_->stream));
+    return 0;
+  }
+
+  int sync() {
+    GI_CUDA_TRY(cudaStreamSynchronize(ws_->stream));
+    return 0;
+  }
+
+  // _refresh_state: returns loss, max|g|, g_cov, g on the support
+  int refresh(const std::vector<int64_t>& sup, const std::vector<double>& w,
+              const std::vector<double>& bcov, double& loss, double& gmax,
+              std::vector<double>& gcov, std::vector<double>& gsup) {
+    const gi::MatrixDesc d = h_->desc();
+    cudaStream_t s = ws_->stream;
+    const bool has_fit = !sup.empty();
+    if (has_fit) {
+      // the upload buffers are reused below for the gather, so sync the ax inputs first
+      TRY(upload_sparse(sup, w));
+      TRY(gi::launch_ax(d, ws_->u, ws_->v, ws_->didx, ws_->dw, (int64_t)sup.size(), ws_->fitb, 0,
+                        s));
+      ++launches;
+    }
+    TRY(upload_cov(bcov));
+    const uint8_t* keep = masked_ ? ws_->keep : nullptr;
+    TRY(gi::launch_residual(ws_->n, ws_->y, has_fit ? ws_->fitb : nullptr,
+                            ws_->c ? ws_->C : nullptr, (int)ws_->c, ws_->cvec, keep, n_eff_,
+                            ws_->r, ws_->scal, ws_->partials, ws_->ticket, s));
+    TRY(gi::launch_center(ws_->n, ws_->npad, ws_->r, keep, ws_->scal, ws_->rt, ws_->partials,
+                          ws_->ticket, s));
+    launches += 2;
+    if (ws_->p) {
+      if (ev0) GI_CUDA_TRY(cudaEventRecord(ev0, s));
+      TRY(gi::launch_aty_fast(d, static_cast<const uint8_t*>(h_->gmiss->ptr), ws_->rt, ws_->u,
+                              ws_->v, ws_->s1cnt, ws_->scal, -1.0, ws_->g, h_->sms, s));
+      if (ev1) GI_CUDA_TRY(cudaEventRecord(ev1, s));
+      ++aty_launches;
+      TRY(gi::launch_maxabs(ws_->p, ws_->g, ws_->scal, 3, ws_->partials, ws_->ticket, s));
+      launches += 2;
+    }
+    if (ws_->c) {
+      TRY(gi::launch_covgrad(ws_->n, ws_->C, (int)ws_->c, ws_->r, ws_->cvec + ws_->c,
+                             ws_->partials, ws_->ticket, s));
+      ++launches;
+    }
+    const int64_t ks = (int64_t)sup.size();
+    if (ks) {
+      // didx still holds the support (uploaded above, stream-ordered)
+      TRY(gi::launch_gather(ks, ws_->didx, ws_->g, ws_->oval, s));
+      ++launches;
+    }
+    double* ho = ws_->hout;
+    GI_CUDA_TRY(cudaMemcpyAsync(ho, ws_->scal, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
+    if (ws_->c)
+      GI_CUDA_TRY(cudaMemcpyAsync(ho + 8, ws_->cvec + ws_->c, sizeof(double) * ws_->c,
+                                  cudaMemcpyDeviceToHost, s));
+    if (ks)
+      GI_CUDA_TRY(cudaMemcpyAsync(ho + 8 + ws_->c, ws_->oval, sizeof(double) * ks,
+                                  cudaMemcpyDeviceToHost, s));
+    TRY(sync());
+    if (ev0 && ws_->p) {
+      float ms = 0.f;
+      GI_CUDA_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
+      aty_ms += ms;
+    }
+    loss = ho[0];
+    gmax = ws_->p ? ho[3] : 0.0;
+    gcov.assign(ho + 8, ho + 8 + ws_->c);
+    gsup.assign(ho + 8 + ws_->c, ho + 8 + ws_->c + ks);
+    return 0;
+  }
+
+  // || X_idx w + C wcov ||^2 over the view's rows
+  int image_sumsq(const std::vector<int64_t>& idx, const std::vector<double>& w,
+                  const std::vector<double>* wcov, double& out) {
+    const gi::MatrixDesc d = h_->desc();
+    cudaStream_t s = ws_->stream;
+    TRY(upload_sparse(idx, w));
+    TRY(gi::launch_ax(d, ws_->u, ws_->v, ws_->didx, ws_->dw, (int64_t)idx.size(), ws_->img, 0, s));
+    ++launches;
+    if (wcov && ws_->c) {
+      TRY(upload_cov(*wcov));
+      TRY(gi::launch_add_cov(ws_->n, ws_->C, (int)ws_->c, ws_->cvec, ws_->img, s));
+      ++launches;
+    }
+    if (masked_) {
+      TRY(gi::launch_mask(ws_->n, ws_->keep, ws_->img, s));
+      ++launches;
+    }
+    TRY(gi::launch_sumsq(ws_->n, ws_->img, ws_->scal, 4, ws_->partials, ws_->ticket, s));
+    ++launches;
+    GI_CUDA_TRY(cudaMemcpyAsync(ws_->hout, ws_->scal + 4, sizeof(double), cudaMemcpyDeviceToHost,
+                                s));
+    TRY(sync());
+    out = ws_->hout[0];
+    return 0;
+  }
+
+  // k largest |g| (mode 0) or |beta - mu g| (mode 1), sorted by index
+  int topk(int mode, double mu, int64_t k, std::vector<Pair>& out) {
+    out.clear();
+    if (ws_->p == 0 || k <= 0) return 0;
+    const int64_t ke = std::min(k, ws_->kcap);
+    cudaStream_t s = ws_->stream;
+    TRY(gi::launch_topk(ws_->p, ke, mode, ws_->beta, ws_->g, mu, 0, ws_->ckey, ws_->cidx,
+                        ws_->cval, ws_->oidx, ws_->oval, nullptr, ws_->ocnt, s));
+    launches += 2;
+    double* ho = ws_->hout;
+    GI_CUDA_TRY(cudaMemcpyAsync(ho, ws_->ocnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    GI_CUDA_TRY(cudaMemcpyAsync(ho + 1, ws_->oidx, sizeof(int64_t) * ke, cudaMemcpyDeviceToHost, s));
+    GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + ke, ws_->oval, sizeof(double) * ke,
+                                cudaMemcpyDeviceToHost, s));
+    TRY(sync());
+    int64_t cnt = 0;
+    memcpy(&cnt, ho, sizeof(int64_t));
+    const int64_t* hi = reinterpret_cast<const int64_t*>(ho + 1);
+    out.resize((size_t)cnt);
+    for (int64_t t = 0; t < cnt; ++t) out[t] = Pair{hi[t], ho[1 + ke + t]};
+    std::sort(out.begin(), out.end(), [](const Pair& a, const Pair& b) { return a.idx < b.idx; });
+    return 0;
+  }
+
+  int scatter_beta(const std::vector<int64_t>& idx, const std::vector<double>& w) {
+    if (idx.empty()) return 0;
+    TRY(upload_sparse(idx, w));
+    TRY(gi::launch_scatter((int64_t)idx.size(), ws_->didx, ws_->dw, ws_->beta, ws_->stream));
+    ++launches;
+    return sync();  // the upload staging is reused by the next phase
+  }
+
+ private:
+  gi_matrix* h_;
+  FitWs* ws_;
+  gi_fit_config cfg_;
+  bool masked_;
+  double n_eff_;
+};
+
+double dot(const std::vector<double>& a) {
+  double s = 0.0;
+  for (double x : a) s += x * x;
+  return s;
+}
+
+bool any_nonzero(const std::vector<double>& a) {
+  for (double x : a)
+    if (x != 0.0) return true;
+  return false;
+}
+
+}  // namespace
+
+extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
+                      const uint8_t* keep, const double* u, const double* v,
+                      const gi_fit_config* cfg, const int64_t* warm_idx, const double* warm_w,
+                      int64_t warm_k, const double* bcov0, gi_fit_result* res) {
+  CHECK_ARG(h && cfg && res, "NULL argument");
+  CHECK_ARG(c >= 0 && c <= 8, "the native loop supports at most 8 covariate columns");
+  CHECK_ARG(c == 0 || C != nullptr, "covariate matrix is NULL");
+  CHECK_ARG(cfg->k >= 0 && cfg->max_iter >= 1, "invalid solver configuration");
+  CHECK_ARG(res->trace_cap >= cfg->max_iter + 1, "loss trace buffer is too small");
+  CHECK_ARG(res->support_cap >= std::max<int64_t>(cfg->k, warm_k), "support buffer too small");
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard guard(h->device);
+  const int64_t kcap = std::max<int64_t>(std::max<int64_t>(cfg->k, warm_k), 1);
+
+  // workspace cached on the handle (same shape: reused without reallocation)
+  std::shared_ptr<FitWs> ws = std::static_pointer_cast<FitWs>(h->fit_ws);
+  if (!ws || ws->c != c || ws->kcap < kcap || ws->n != h->n) {
+    h->fit_ws.reset();
+    ws.reset();
+    TRY(make_ws(h, c, kcap, ws));
+    h->fit_ws = ws;
+  }
+  cudaStream_t s = ws->stream;
+  const int64_t n = h->n, p = h->p;
+  double n_eff = (double)n;
+  const bool masked = keep != nullptr || (y == nullptr && ws->masked);
+  const gi::MatrixDesc d = h->desc();
+  if (y == nullptr) {
+    // inputs already resident from the previous call on this handle (benchmarks)
+    CHECK_ARG(ws->primed, "gi_fit with y == NULL needs a previous call on this handle");
+    n_eff = ws->n_eff;
+    GI_CUDA_TRY(cudaMemsetAsync(ws->beta, 0, sizeof(double) * std::max<int64_t>(p, 1), s));
+    GI_CUDA_TRY(cudaStreamSynchronize(s));
+  } else {
+  // ---- inputs
+  GI_CUDA_TRY(cudaMemcpyAsync(ws->y, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  if (c) GI_CUDA_TRY(cudaMemcpyAsync(ws->C, C, sizeof(double) * n * c, cudaMemcpyHostToDevice, s));
+  if (masked) {
+    GI_CUDA_TRY(cudaMemcpyAsync(ws->keep, keep, (size_t)n, cudaMemcpyHostToDevice, s));
+    std::vector<uint32_t> mask((size_t)(ws->npad / 16), 0u);
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n; ++i)
+      if (keep[i]) {
+        mask[(size_t)(i >> 4)] |= 1u << (2 * (i & 15));
+        ++cnt;
+      }
+    n_eff = (double)cnt;
+    GI_CUDA_TRY(cudaMemcpyAsync(ws->rowmask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice,
+                                s));
+    // per-SNP counts over the kept rows (its u, v outputs are overwritten below)
+    TRY(gi::launch_stats(d, ws->rowmask, ws->u, ws->v, nullptr, ws->s1cnt, s));
+  } else {
+    GI_CUDA_TRY(cudaMemcpyAsync(ws->s1cnt, h->s1cnt->ptr, sizeof(int32_t) * 2 * p,
+                                cudaMemcpyDeviceToDevice, s));
+  }
+  if (u && v) {
+    GI_CUDA_TRY(cudaMemcpyAsync(ws->u, u, sizeof(double) * p, cudaMemcpyHostToDevice, s));
+    GI_CUDA_TRY(cudaMemcpyAsync(ws->v, v, sizeof(double) * p, cudaMemcpyHostToDevice, s));
+  } else {
+    GI_CUDA_TRY(cudaMemcpyAsync(ws->u, h->du(), sizeof(double) * p, cudaMemcpyDeviceToDevice, s));
+    GI_CUDA_TRY(cudaMemcpyAsync(ws->v, h->dv(), sizeof(double) * p, cudaMemcpyDeviceToDevice, s));
+  }
+  GI_CUDA_TRY(cudaMemsetAsync(ws->beta, 0, sizeof(double) * std::max<int64_t>(p, 1), s));
+  GI_CUDA_TRY(cudaStreamSynchronize(s));
+  ws->primed = true;
+  ws->masked = masked;
+  ws->n_eff = n_eff;
+  }
+
+  NativeFit F(h, ws.get(), cfg, masked, n_eff);
+  struct EventPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~EventPair() {
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } evs;
+  if (cfg->flags & 1) {
+    GI_CUDA_TRY(cudaEventCreate(&evs.a));
+    GI_CUDA_TRY(cudaEventCreate(&evs.b));
+    F.ev0 = evs.a;
+    F.ev1 = evs.b;
+  }
+  // ---- initial_state (iht.py:194-215): warm support or zero; b_cov from the caller
+  std::vector<int64_t> sup;
+  std::vector<double> w;
+  for (int64_t t = 0; t < warm_k; ++t)
+    if (warm_w[t] != 0.0) {
+      sup.push_back(warm_idx[t]);
+      w.push_back(warm_w[t]);
+    }
+  std::vector<double> bcov(bcov0, bcov0 + c);
+  TRY(F.scatter_beta(sup, w));
+  double loss = 0.0, gmax = 0.0;
+  std::vector<double> gcov, gsup;
+  TRY(F.refresh(sup, w, bcov, loss, gmax, gcov, gsup));
+  int64_t trace_len = 0;
+  res->loss_trace[trace_len++] = loss;
+  int64_t iterations = 0, total_bt = 0;
+  int reason = 1;  // max-iter
+
+  std::vector<Pair> cand;
+  std::vector<int64_t> ridx, new_sup, dsup;
+  std::vector<double> rg, new_w, dval, cand_cov(c), dcov(c);
+  for (int64_t it = 0; it < cfg->max_iter; ++it) {
+    // ---------------------------------------------------------- iht_step
+    double grad_max = gmax;
+    for (double x : gcov) grad_max = std::max(grad_max, std::fabs(x));
+    double step_inf;
+    if (grad_max == 0.0) {
+      step_inf = 0.0;  // fixed point (iht.py:262-267)
+    } else {
+      // restriction (iht.py:218-230)
+      if (!sup.empty() && (any_nonzero(gsup) || any_nonzero(gcov))) {
+        ridx = sup;
+        rg = gsup;
+      } else {
+        TRY(F.topk(0, 0.0, cfg->k, cand));
+        ridx.clear();
+        rg.clear();
+        for (const Pair& q : cand) {
+          ridx.push_back(q.idx);
+          rg.push_back(q.val);
+        }
+      }
+      if (ridx.empty() && !(c && any_nonzero(gcov))) {
+        step_inf = 0.0;  // k = 0 with settled covariates (iht.py:270-275)
+      } else {
+        // mu (iht.py:233-244)
+        const double num = dot(rg) + dot(gcov);
+        if (num == 0.0) {
+          gi_set_error("gradient vanishes on the restriction; nothing to step on");
+          return -2;
+        }
+        double den = 0.0;
+        TRY(F.image_sumsq(ridx, rg, c ? &gcov : nullptr, den));
+        if (den == 0.0 || !std::isfinite(den)) {
+          gi_set_error("degenerate active set: restricted columns have zero image");
+          return -3;
+        }
+        double mu = num / den;
+        bool accepted = false;
+        int64_t bt = 0;
+        for (int64_t tries = 0; tries <= cfg->max_backtracks; ++tries) {
+          TRY(F.topk(1, mu, cfg->k, cand));
+          new_sup.clear();
+          new_w.clear();
+          for (const Pair& q : cand)
+            if (q.val != 0.0) {
+              new_sup.push_back(q.idx);
+              new_w.push_back(q.val);
+            }
+          for (int64_t l = 0; l < c; ++l) {
+            cand_cov[l] = bcov[l] - mu * gcov[l];
+            dcov[l] = cand_cov[l] - bcov[l];
+          }
+          // delta over the union of old and new supports, ascending (iht.py:283-285)
+          dsup.clear();
+          dval.clear();
+          size_t a = 0, b = 0;
+          while (a < sup.size() || b < new_sup.size()) {
+            int64_t j;
+            double oldv = 0.0, newv = 0.0;
+            if (b >= new_sup.size() || (a < sup.size() && sup[a] < new_sup[b])) {
+              j = sup[a];
+              oldv = w[a++];
+            } else if (a >= sup.size() || new_sup[b] < sup[a]) {
+              j = new_sup[b];
+              newv = new_w[b++];
+            } else {
+              j = sup[a];
+              oldv = w[a++];
+              newv = new_w[b++];
+            }
+            const double dd = newv - oldv;
+            if (dd != 0.0) {
+              dsup.push_back(j);
+              dval.push_back(dd);
+            }
+          }
+          const double dsq = dot(dval) + dot(dcov);
+          if (dsq == 0.0 || new_sup == ridx) {
+            accepted = true;
+            break;
+          }
+          double xdsq = 0.0;
+          TRY(F.image_sumsq(dsup, dval, c ? &dcov : nullptr, xdsq));
+          if (xdsq == 0.0) {
+            accepted = true;
+            break;
+          }
+          const double omega = (1.0 - cfg->c_omega) * dsq / xdsq;
+          if (mu < omega) {
+            accepted = true;
+            break;
+          }
+          mu *= 0.5;
+          ++bt;
+        }
+        total_bt += bt;
+        if (!accepted) {
+          reason = 2;  // step-size collapse; the state is not updated
+          break;
+        }
+        step_inf = 0.0;
+        for (double x : dval) step_inf = std::max(step_inf, std::fabs(x));
+        for (double x : dcov) step_inf = std::max(step_inf, std::fabs(x));
+        // beta <- candidate; refresh (iht.py:311-321)
+        std::vector<double> zeros(sup.size(), 0.0);
+        TRY(F.scatter_beta(sup, zeros));
+        TRY(F.scatter_beta(new_sup, new_w));
+        sup = new_sup;
+        w = new_w;
+        bcov = cand_cov;
+        TRY(F.refresh(sup, w, bcov, loss, gmax, gcov, gsup));
+      }
+    }
+    ++iterations;
+    res->loss_trace[trace_len++] = loss;
+    if (!std::isfinite(loss)) {
+      gi_set_error("loss diverged to a non-finite value");
+      return -4;
+    }
+    if (step_inf < cfg->tol) {
+      reason = 0;
+      break;
+    }
+  }
+  // ---- model (SparseModel.from_parts: nonzero weights, sorted)
+  int64_t nnz = 0;
+  for (size_t t = 0; t < sup.size(); ++t)
+    if (w[t] != 0.0) {
+      res->support[nnz] = sup[t];
+      res->weights[nnz] = w[t];
+      ++nnz;
+    }
+  res->nnz = nnz;
+  for (int64_t l = 0; l < c; ++l) res->covar[l] = bcov[l];
+  res->trace_len = trace_len;
+  res->iterations = iterations;
+  res->reason = reason;
+  res->backtracks = total_bt;
+  res->kernel_launches = F.launches;
+  res->aty_ms_total = F.aty_ms;
+  res->aty_launches = F.aty_launches;
+  return 0;
+}

@@ -54,7 +54,24 @@ __device__ __forceinline__ void block_sum(double (&x)[NV], double* sh) {
   __syncthreads();
 }
 
-// returns true in thread 0 of the last block to arrive
+// Deterministic fold of per-block partials by the first warp of the last
+// block: lane l sums partials l, l+32, ... in order, then a fixed xor tree.
+__device__ __forceinline__ double fold_sum(const double* partials, int stride, int slot,
+                                           unsigned nblocks) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (unsigned b = lane; b < nblocks; b += 32) s += partials[b * stride + slot];
+  return warp_sum(s);
+}
+
+__device__ __forceinline__ double fold_max(const double* partials, unsigned nblocks) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (unsigned b = lane; b < nblocks; b += 32) s = fmax(s, partials[b]);
+  return warp_max(s);
+}
+
+// returns true in every thread of the last block to arrive
 __device__ __forceinline__ bool last_block(unsigned int* ticket) {
   __shared__ bool is_last;
   __threadfence();
@@ -97,15 +114,14 @@ __global__ void residual_kernel(int64_t n, const double* __restrict__ y,
     ws.partials[blockIdx.x * 2] = acc[0];
     ws.partials[blockIdx.x * 2 + 1] = acc[1];
   }
-  if (last_block(ws.ticket) && threadIdx.x == 0) {
-    double s2 = 0.0, s1 = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-      s2 += ws.partials[b * 2];
-      s1 += ws.partials[b * 2 + 1];
+  if (last_block(ws.ticket) && threadIdx.x < 32) {
+    const double s2 = fold_sum(ws.partials, 2, 0, gridDim.x);
+    const double s1 = fold_sum(ws.partials, 2, 1, gridDim.x);
+    if (threadIdx.x == 0) {
+      scal[0] = 0.5 * s2;
+      scal[1] = n_eff > 0.0 ? s1 / n_eff : 0.0;
+      *ws.ticket = 0u;
     }
-    scal[0] = 0.5 * s2;
-    scal[1] = n_eff > 0.0 ? s1 / n_eff : 0.0;
-    *ws.ticket = 0u;
   }
 }
 
@@ -125,11 +141,12 @@ __global__ void center_kernel(int64_t n, int64_t n_pad, const double* __restrict
   }
   block_sum<1>(acc, sh);
   if (threadIdx.x == 0) ws.partials[blockIdx.x] = acc[0];
-  if (last_block(ws.ticket) && threadIdx.x == 0) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += ws.partials[b];
-    scal[2] = s;
-    *ws.ticket = 0u;
+  if (last_block(ws.ticket) && threadIdx.x < 32) {
+    const double s = fold_sum(ws.partials, 1, 0, gridDim.x);
+    if (threadIdx.x == 0) {
+      scal[2] = s;
+      *ws.ticket = 0u;
+    }
   }
 }
 
@@ -151,13 +168,12 @@ __global__ void covgrad_kernel(int64_t n, const double* __restrict__ C, int c,
   block_sum<8>(acc, sh);
   if (threadIdx.x == 0)
     for (int l = 0; l < 8; ++l) ws.partials[blockIdx.x * 8 + l] = acc[l];
-  if (last_block(ws.ticket) && threadIdx.x == 0) {
+  if (last_block(ws.ticket) && threadIdx.x < 32) {
     for (int l = 0; l < c; ++l) {
-      double s = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) s += ws.partials[b * 8 + l];
-      gcov[l] = -s;
+      const double s = fold_sum(ws.partials, 8, l, gridDim.x);
+      if (threadIdx.x == 0) gcov[l] = -s;
     }
-    *ws.ticket = 0u;
+    if (threadIdx.x == 0) *ws.ticket = 0u;
   }
 }
 
@@ -176,11 +192,12 @@ __global__ void maxabs_kernel(int64_t m, const double* __restrict__ x, double* _
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
     ws.partials[blockIdx.x] = mx;
   }
-  if (last_block(ws.ticket) && threadIdx.x == 0) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s = fmax(s, ws.partials[b]);
-    scal[slot] = s;
-    *ws.ticket = 0u;
+  if (last_block(ws.ticket) && threadIdx.x < 32) {
+    const double s = fold_max(ws.partials, gridDim.x);
+    if (threadIdx.x == 0) {
+      scal[slot] = s;
+      *ws.ticket = 0u;
+    }
   }
 }
 
@@ -194,11 +211,12 @@ __global__ void sumsq_kernel(int64_t m, const double* __restrict__ x, double* __
     acc[0] += x[i] * x[i];
   block_sum<1>(acc, sh);
   if (threadIdx.x == 0) ws.partials[blockIdx.x] = acc[0];
-  if (last_block(ws.ticket) && threadIdx.x == 0) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += ws.partials[b];
-    scal[slot] = s;
-    *ws.ticket = 0u;
+  if (last_block(ws.ticket) && threadIdx.x < 32) {
+    const double s = fold_sum(ws.partials, 1, 0, gridDim.x);
+    if (threadIdx.x == 0) {
+      scal[slot] = s;
+      *ws.ticket = 0u;
+    }
   }
 }
 
@@ -317,23 +335,46 @@ __device__ void block_select(int64_t m, int64_t k, Get get, uint64_t& thr_key,
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int64_t need = s_kk;
-      int bin = 255;
-      for (; bin >= 0; --bin) {
-        if ((int64_t)hist[bin] >= need) break;
-        need -= hist[bin];
+    if (threadIdx.x < 32) {
+      // warp-parallel search for the boundary bin: lane l owns bins 8l..8l+7;
+      // `above` = number of candidates in bins higher than the lane's range
+      const int lane = threadIdx.x;
+      unsigned c[8];
+      unsigned tot = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        c[q] = hist[8 * lane + q];
+        tot += c[q];
       }
-      if (bin < 0) bin = 0;  // fewer elements than k: everything is taken
-      if (d < 8) {
-        s_key |= (uint64_t)bin << (56 - 8 * d);
-        s_kmask |= (uint64_t)255u << (56 - 8 * d);
-      } else {
-        s_sec |= (uint32_t)bin << (24 - 8 * (d - 8));
-        s_smask |= 255u << (24 - 8 * (d - 8));
+      unsigned incl = tot;  // inclusive suffix sum over lanes >= lane
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_down_sync(0xffffffffu, incl, o);
+        if (lane + o < 32) incl += t;
       }
-      s_kk = need;
-      if ((int64_t)hist[bin] == need) s_done = 1;
+      const unsigned above = incl - tot;
+      const int64_t need0 = s_kk;
+      // the boundary lane: above < need0 <= above + tot (or lane 0 if total < need0)
+      const bool mine = ((int64_t)above < need0 && need0 <= (int64_t)(above + tot)) ||
+                        (lane == 0 && (int64_t)incl < need0);
+      if (mine) {
+        int64_t need = need0 - (int64_t)above;
+        int bin = 8 * lane + 7;
+        for (int q = 7; q >= 0; --q) {
+          bin = 8 * lane + q;
+          if ((int64_t)c[q] >= need) break;
+          need -= c[q];
+        }
+        if (d < 8) {
+          s_key |= (uint64_t)bin << (56 - 8 * d);
+          s_kmask |= (uint64_t)255u << (56 - 8 * d);
+        } else {
+          s_sec |= (uint32_t)bin << (24 - 8 * (d - 8));
+          s_smask |= 255u << (24 - 8 * (d - 8));
+        }
+        s_kk = need;
+        if ((int64_t)hist[bin] == need) s_done = 1;
+      }
     }
     __syncthreads();
     if (s_done) break;
@@ -458,6 +499,20 @@ int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double
   GI_LAUNCH_CHECK();
   topk_merge_kernel<<<1, 1024, 0, s>>>(nb * k, k, cand_key, cand_idx, cand_val, out_idx,
                                        out_val, out_key, out_count);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+// x[i] = keep[i] ? x[i] : 0
+__global__ void mask_kernel(int64_t n, const uint8_t* __restrict__ keep, double* __restrict__ x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!keep[i]) x[i] = 0.0;
+}
+
+int launch_mask(int64_t n, const uint8_t* keep, double* x, cudaStream_t s) {
+  if (n <= 0) return 0;
+  mask_kernel<<<red_grid(n), kRedThreads, 0, s>>>(n, keep, x);
   GI_LAUNCH_CHECK();
   return 0;
 }

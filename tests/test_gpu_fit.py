@@ -46,8 +46,9 @@ def test_fit_matches_reference(name):
                 case["iterations"], case["reason"])
 
 
+@pytest.mark.parametrize("native", [True, False], ids=["native-loop", "python-loop"])
 @pytest.mark.parametrize("seed", range(12))
-def test_fit_matches_oracle_random(seed):
+def test_fit_matches_oracle_random(seed, native):
     rng = np.random.default_rng(100 + seed)
     n = int(rng.integers(60, 900))
     p = int(rng.integers(50, 3000))
@@ -65,12 +66,13 @@ def test_fit_matches_oracle_random(seed):
     support = np.sort(rng.choice(p, min(k, 5), replace=False))
     y = ref.geno.ax_columns(support, rng.standard_normal(support.size)) + rng.normal(0, 0.2, n)
     want = oracle.fit(ref, y, k)
-    got = gi.fit(view, y, gi.IhtConfig(k=k))
+    got = gi.fit(view, y, gi.IhtConfig(k=k), native=native)
     _assert_fit(got, want.support, want.weights, want.covar, want.loss_trace, want.iterations,
                 want.reason)
 
 
-def test_warm_start_and_collapse():
+@pytest.mark.parametrize("native", [True, False], ids=["native-loop", "python-loop"])
+def test_warm_start_and_collapse(native):
     gi = _gi()
     codes = oracle.random_codes(120, 40, seed=4, missing_rate=0.0)
     m = gi.PackedGenotypeMatrix.from_codes(codes)
@@ -78,12 +80,13 @@ def test_warm_start_and_collapse():
     ref = oracle.OracleView(oracle.OraclePacked.from_codes(codes), None)
     y = ref.geno.ax_columns(np.array([3]), np.array([2.0]))
     warm = gi.SparseModel.from_parts([11], [1.0], np.zeros(0), k=1, p=40)
-    got = gi.fit(view, y, gi.IhtConfig(k=1, c_omega=0.99, max_backtracks=0), warm=warm)
+    got = gi.fit(view, y, gi.IhtConfig(k=1, c_omega=0.99, max_backtracks=0), warm=warm,
+                 native=native)
     want = oracle.fit(ref, y, 1, c_omega=0.99, max_backtracks=0,
                       warm=(np.array([11]), np.array([1.0]), np.zeros(0)))
     assert got.reason == want.reason
     assert got.iterations == want.iterations
-    got2 = gi.fit(view, y, gi.IhtConfig(k=2), warm=warm)
+    got2 = gi.fit(view, y, gi.IhtConfig(k=2), warm=warm, native=native)
     want2 = oracle.fit(ref, y, 2, warm=(np.array([11]), np.array([1.0]), np.zeros(0)))
     _assert_fit(got2, want2.support, want2.weights, want2.covar, want2.loss_trace,
                 want2.iterations, want2.reason)
@@ -105,3 +108,43 @@ def test_cv_matches_reference(name):
     np.testing.assert_array_equal(rep.final_model.support, case["final_support"])
     np.testing.assert_allclose(rep.final_model.weights, case["final_weights"], rtol=RTOL)
     np.testing.assert_allclose(rep.final_model.covar, case["final_covar"], rtol=RTOL, atol=1e-12)
+
+
+def test_errors_and_fixed_points():
+    gi = _gi()
+    codes = oracle.random_codes(40, 30, seed=5, missing_rate=0.1)
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=40))
+    # zero response: fixed point after one iteration (test_iht.py:179-184)
+    res = gi.fit(view, np.zeros(40), gi.IhtConfig(k=3))
+    assert res.iterations == 1 and res.converged and res.model.nnz == 0
+    with pytest.raises(ValueError):
+        gi.fit(view, np.full(40, np.nan), gi.IhtConfig(k=1))
+    with pytest.raises(ValueError):
+        gi.fit(view, np.zeros(39), gi.IhtConfig(k=1))
+    # monomorphic column alone in the restriction -> degenerate (test_iht.py:113-124)
+    codes2 = np.full((12, 3), 2, np.uint8)
+    codes2[:, 0] = oracle.random_codes(12, 1, seed=1)[:, 0]
+    v2 = gi.StandardizedView(gi.PackedGenotypeMatrix.from_codes(codes2), None)
+    warm = gi.SparseModel.from_parts([1], [1.0], np.zeros(0), k=1, p=3)
+    y = np.random.default_rng(3).standard_normal(12)
+    for native in (True, False):
+        try:
+            gi.fit(v2, y, gi.IhtConfig(k=1), warm=warm, native=native)
+        except ValueError as exc:
+            assert "degenerate" in str(exc) or "vanishes" in str(exc)
+
+
+def test_cv_errors():
+    gi = _gi()
+    codes = oracle.random_codes(30, 40, seed=6)
+    view = gi.StandardizedView(gi.PackedGenotypeMatrix.from_codes(codes),
+                               gi.CovariateBlock.build(None, n=30))
+    plan = gi.CvPlan.build(30, 3, np.arange(1, 25), seed=1)
+    with pytest.raises(ValueError, match="training fold"):
+        gi.cv_iht(view, np.zeros(30), plan, gi.IhtConfig(k=24))
+    y = np.zeros(30)
+    y[0] = np.inf
+    plan2 = gi.CvPlan.build(30, 3, np.array([1, 2]), seed=2)
+    with pytest.raises(RuntimeError, match=r"fold \d, k=1"):
+        gi.cv_iht(view, y, plan2, gi.IhtConfig(k=2))
