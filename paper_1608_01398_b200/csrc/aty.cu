@@ -403,6 +403,7 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
                     const double* d_scal, double scale, double* out, int num_sms,
                     cudaStream_t s) {
   if (m.p == 0) return 0;
+
   static bool configured = false;
   if (!configured) {
     const char* env = getenv("GI_ATY_FLAGS");

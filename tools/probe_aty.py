@@ -28,6 +28,7 @@ r = torch.zeros(npad, dtype=torch.float32, device="cuda")
 r[: a.n] = torch.as_tensor(rng.standard_normal(a.n), dtype=torch.float32)
 rd = r.double()
 srt = torch.tensor([float(r.double().sum())], dtype=torch.float64, device="cuda")
+scal = torch.tensor([0.0, 0.0, float(r.double().sum()), 0.0], dtype=torch.float64, device="cuda")
 g = torch.zeros(a.p, dtype=torch.float64, device="cuda")
 s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 P = _native.ptr
@@ -37,7 +38,7 @@ def launch():
     if a.exact:
         check(lib().gi_dev_aty_exact(m.handle, None, None, P(rd), P(srt), 1.0, P(g), s))
     else:
-        check(lib().gi_dev_aty_fast(m.handle, None, None, P(r), P(srt), 1.0, P(g), s))
+        check(lib().gi_dev_aty_fast(m.handle, None, None, None, P(r), P(scal), 1.0, P(g), s))
 
 
 for _ in range(3):
