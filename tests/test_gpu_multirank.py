@@ -1,0 +1,77 @@
+"""The sharded DEVICE path on one GPU: two processes, each owning a contiguous
+SNP block (its own device-resident shard and DeviceEngine), joined by gloo.
+Collectives are host-staged, so no kernel waits on another process.  The
+sharded fit must reproduce the unsharded device fit and the oracle: identical
+support and iteration count, weights and loss to 1e-6."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+N, P, K, SEED = 3000, 20011, 12, 77
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1608_01398_b200 as gi
+        from paper_1608_01398_b200.dist import ShardedGenotypes, TorchComm
+        from paper_1608_01398_b200.simulate import SimulationSpec, simulate_phenotype
+
+        torch.cuda.set_device(0)
+        comm = TorchComm()
+        geno = ShardedGenotypes.synthetic(N, P, SEED, comm, device=0, missing_rate=0.01)
+        view = gi.StandardizedView(geno, gi.CovariateBlock.build(None, n=N))
+        y, truth = simulate_phenotype(view, SimulationSpec(k_true=K, seed=5))
+        res = gi.fit(view, y, gi.IhtConfig(k=K))
+        q.put((rank, y, res.model.support, res.model.weights, res.model.covar, res.loss_trace,
+               res.iterations, res.reason))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_shards_on_one_gpu_match_single_device_fit():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    out = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p_ in procs:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    import paper_1608_01398_b200 as gi
+
+    y = out[0][1]
+    np.testing.assert_array_equal(out[1][1], y)
+    full = gi.PackedGenotypeMatrix.synthetic(N, P, SEED, missing_rate=0.01)
+    view = gi.StandardizedView(full, gi.CovariateBlock.build(None, n=N))
+    want = gi.fit(view, y, gi.IhtConfig(k=K))
+    ref = oracle.fit(oracle.OracleView(oracle.OraclePacked.from_bed(np.array(full.data), N),
+                                       oracle.intercept(N)), y, K)
+    np.testing.assert_array_equal(want.model.support, ref.support)
+    assert want.iterations == ref.iterations
+    for rank, _, support, weights, covar, trace, iters, reason in out:
+        np.testing.assert_array_equal(support, want.model.support)
+        assert iters == want.iterations and reason == want.reason
+        np.testing.assert_allclose(weights, want.model.weights, rtol=1e-6)
+        np.testing.assert_allclose(covar, want.model.covar, rtol=1e-6, atol=1e-12)
+        np.testing.assert_allclose(trace, want.loss_trace, rtol=1e-6)
