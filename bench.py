@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--cpu-slice", type=int, default=0,
                     help="SNPs in the CPU-baseline sample (0 = auto, ~2.5 GB)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2path", "c4cv"],
+                    help="c3 (default, the metric's config), c2path (BASELINE config 2: "
+                         "k=10..50 model-size path at n=5k x p=100k), c4cv (config 4: "
+                         "5-fold CV over k=1..20 at n=20k x p=500k)")
     return ap.parse_args()
 
 
@@ -206,10 +210,121 @@ def reference_arm(a):
 
 
 # ------------------------------------------------------------------ GPU leg
+def secondary(a):
+    """Model-size path (config 2) or cross-validation (config 4), 1 GPU.
+
+    One step = the whole path / the whole CV; value = IHT iterations per second
+    over it (all fits run concurrently on the device, one stream each).  The
+    CPU baseline runs the oracle (reference algorithm) on the same bytes: the
+    full path for config 2 (and checks supports/iterations), a bounded sample
+    of fits for config 4."""
+    import torch
+
+    import paper_1608_01398_b200 as gi
+    from paper_1608_01398_b200.simulate import SimulationSpec, simulate_phenotype
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    if a.workload == "c2path":
+        n, p, k_true, path = 5000, 100_000, 20, np.arange(10, 51)
+    else:
+        n, p, k_true, path = 20_000, 500_000, 10, np.arange(1, 21)
+    m = gi.PackedGenotypeMatrix.synthetic(n, p, a.seed, missing_rate=a.missing)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=n))
+    y, _ = simulate_phenotype(view, SimulationSpec(k_true=k_true, seed=a.pheno_seed))
+    stream = torch.cuda.current_stream()
+
+    def run():
+        if a.workload == "c2path":
+            res = gi.fit_path(view, y, path)
+            return sum(r.iterations for r in res), res
+        plan = gi.CvPlan.build(n, 5, path, seed=2016)
+        rep = gi.cv_iht(view, y, plan, gi.IhtConfig(k=int(path.max())))
+        return None, rep
+
+    for _ in range(a.warmup):
+        run()
+    iters_per_step = None
+    with ClockSampler(0) as clocks:
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            iters_per_step, out = run()
+        torch.cuda.synchronize()  # every fit stream has drained before e1
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    line = {"metric": METRIC, "unit": "it/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64 (fp32 lookup tables)", "data": "synthetic",
+            "clocks": clocks.summary()}
+    data = np.array(m.data)
+    ref = oracle.OraclePacked.from_bed(data, n)
+    oracle.set_threads(os.cpu_count() or 1)
+    rview = oracle.OracleView(ref, oracle.intercept(n))
+    if a.workload == "c2path":
+        line["config"] = {"workload": f"BASELINE config 2: n={n} x p={p}, model-size path "
+                                      f"k=10..50 (41 cold fits), k_true={k_true}",
+                          "step": "all 41 fits of the path"}
+        line["value"] = iters_per_step / (ms / 1e3)
+        line["fits_per_s"] = path.size / (ms / 1e3)
+        t0 = time.perf_counter()
+        want = [oracle.fit(rview, y, int(k)) for k in path]
+        t_cpu = time.perf_counter() - t0
+        cpu_iters = sum(w.iterations for w in want)
+        line["cpu_baseline"] = {"value": cpu_iters / t_cpu, "unit": "it/s",
+                                "cores": os.cpu_count(), "kind": "port",
+                                "sample": "the full 41-fit path on the oracle (C restatement "
+                                          "of genoiht's kernels + its solver)",
+                                "seconds": t_cpu}
+        line["parity"] = {
+            "supports_equal": all(np.array_equal(g.model.support, w.support)
+                                  for g, w in zip(out, want)),
+            "iterations_equal": all(g.iterations == w.iterations for g, w in zip(out, want)),
+            "max_beta_rel_diff": max(float(np.max(np.abs(g.model.weights - w.weights)
+                                                  / np.abs(w.weights))) if w.weights.size else 0.0
+                                     for g, w in zip(out, want))}
+    else:
+        rep = out
+        line["config"] = {"workload": f"BASELINE config 4: n={n} x p={p}, 5-fold CV over "
+                                      f"k=1..20 + final fit and refit, k_true={k_true}, "
+                                      f"fold seed 2016", "step": "one cv_iht call"}
+        line["value"] = None
+        line["cv_seconds"] = ms / 1e3
+        line["k_best"] = int(rep.k_best)
+        # bounded CPU sample: one fold's re-pack (the reference re-packs the
+        # training and test rows of every fold) and one fit at k = k_best
+        labels = gi.make_folds(n, 5, 2016)
+        train, test = np.flatnonzero(labels != 0), np.flatnonzero(labels == 0)
+        t0 = time.perf_counter()
+        g_train = ref.subset_rows(train)
+        ref.subset_rows(test)
+        t_repack = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        fold_fit = oracle.fit(oracle.OracleView(g_train, oracle.intercept(train.size)), y[train],
+                              int(rep.k_best))
+        t_fit = time.perf_counter() - t0
+        t_cv = 5 * t_repack + 101 * t_fit
+        line["cpu_baseline"] = {"value": 1.0 / t_cv, "unit": "cv/s",
+                                "cores": os.cpu_count(), "kind": "port",
+                                "sample": f"oracle: one fold re-pack ({t_repack:.1f} s, x5) + one "
+                                          f"fit at k={rep.k_best} ({fold_fit.iterations} "
+                                          f"iterations, {t_fit:.2f} s, x101 fits); "
+                                          f"extrapolated CV = {t_cv:.0f} s"}
+        line["cv_per_s"] = 1.0 / (ms / 1e3)
+    print(json.dumps(line), flush=True)
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         reference_arm(a)
+        return
+    if a.workload != "c3":
+        secondary(a)
         return
     import torch
 

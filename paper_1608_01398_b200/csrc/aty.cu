@@ -34,6 +34,8 @@
 //   The caller passes the reference's own sum_r (numpy pairwise r.sum()).
 #include <stdlib.h>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace gi {
@@ -404,14 +406,15 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
                     cudaStream_t s) {
   if (m.p == 0) return 0;
 
-  static bool configured = false;
-  if (!configured) {
+  static std::once_flag once;
+  static cudaError_t cfg_err = cudaSuccess;
+  std::call_once(once, [] {
     const char* env = getenv("GI_ATY_FLAGS");
     if (env) g_aty_flags = atoi(env);
-    GI_CUDA_TRY(cudaFuncSetAttribute(aty_fast_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFast));
-    configured = true;
-  }
+    cfg_err = cudaFuncSetAttribute(aty_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemFast);
+  });
+  GI_CUDA_TRY(cfg_err);
   FastArgs a;
   a.m = m;
   a.group_missing = group_missing;

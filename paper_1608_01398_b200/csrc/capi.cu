@@ -156,6 +156,7 @@ int gi_matrix_with_stats(const gi_matrix* src, const double* u, const double* v,
   h->miss_cnt = src->miss_cnt;
   h->gmiss = src->gmiss;
   h->s1cnt = src->s1cnt;
+  h->fit_pool = src->fit_pool;
   DeviceGuard g(h->device);
   GI_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   TRY(alloc(h->u, sizeof(double) * h->p, h->device, false));

@@ -48,18 +48,20 @@ struct FitWs {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
+    for (void* ptr : dev_allocs) cudaFreeAsync(ptr, stream);
     if (stream) cudaStreamSynchronize(stream);
-    for (void* ptr : dev_allocs) cudaFree(ptr);
     if (hin) cudaFreeHost(hin);
     if (hout) cudaFreeHost(hout);
     if (stream) cudaStreamDestroy(stream);
     cudaSetDevice(prev);
   }
 
+  // stream-ordered pool allocations: no device-wide synchronisation, so a new
+  // workspace does not stall fits already running on other streams
   template <typename T>
   int dalloc(T*& out, int64_t count) {
     void* ptr = nullptr;
-    GI_CUDA_TRY(cudaMalloc(&ptr, sizeof(T) * (size_t)std::max<int64_t>(count, 1)));
+    GI_CUDA_TRY(cudaMallocAsync(&ptr, sizeof(T) * (size_t)std::max<int64_t>(count, 1), stream));
     dev_allocs.push_back(ptr);
     out = static_cast<T*>(ptr);
     return 0;
@@ -307,18 +309,37 @@ extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
   CHECK_ARG(cfg->k >= 0 && cfg->max_iter >= 1, "invalid solver configuration");
   CHECK_ARG(res->trace_cap >= cfg->max_iter + 1, "loss trace buffer is too small");
   CHECK_ARG(res->support_cap >= std::max<int64_t>(cfg->k, warm_k), "support buffer too small");
-  std::lock_guard<std::mutex> lock(h->mu);
   DeviceGuard guard(h->device);
   const int64_t kcap = std::max<int64_t>(std::max<int64_t>(cfg->k, warm_k), 1);
 
-  // workspace cached on the handle (same shape: reused without reallocation)
-  std::shared_ptr<FitWs> ws = std::static_pointer_cast<FitWs>(h->fit_ws);
-  if (!ws || ws->c != c || ws->kcap < kcap || ws->n != h->n) {
-    h->fit_ws.reset();
-    ws.reset();
-    TRY(make_ws(h, c, kcap, ws));
-    h->fit_ws = ws;
+  // take a workspace of the right shape from the handle's pool (or make one);
+  // y == NULL (resident inputs) needs one primed by an earlier call
+  std::shared_ptr<FitWs> ws;
+  {
+    std::lock_guard<std::mutex> lock(h->fit_pool->mu);
+    auto& items = h->fit_pool->items;
+    for (size_t i = 0; i < items.size(); ++i) {
+      auto cand = std::static_pointer_cast<FitWs>(items[i]);
+      if (cand->c == c && cand->kcap >= kcap && cand->n == h->n && cand->p == h->p &&
+          (y != nullptr || cand->primed)) {
+        ws = cand;
+        items.erase(items.begin() + (long)i);
+        break;
+      }
+    }
   }
+  if (!ws) {
+    CHECK_ARG(y != nullptr, "gi_fit with y == NULL needs a previous call on this handle");
+    TRY(make_ws(h, c, kcap, ws));
+  }
+  struct PoolReturn {
+    std::shared_ptr<gi_matrix::FitPool> pool;
+    std::shared_ptr<FitWs> ws;
+    ~PoolReturn() {
+      std::lock_guard<std::mutex> lock(pool->mu);
+      pool->items.push_back(ws);
+    }
+  } pool_return{h->fit_pool, ws};
   cudaStream_t s = ws->stream;
   const int64_t n = h->n, p = h->p;
   double n_eff = (double)n;

@@ -6,6 +6,7 @@
 
 #include <memory>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -93,7 +94,14 @@ struct gi_matrix {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   Scratch s_a, s_b, s_c, s_d;
-  std::shared_ptr<void> fit_ws;  // cached workspace of the native fit loop (fit.cu)
+  // workspaces of the native fit loop (fit.cu): a pool, so independent fits on
+  // one matrix run concurrently, each on its own stream.  Shared with the
+  // with_stats copies (a workspace depends on the shape, not on the stats).
+  struct FitPool {
+    std::mutex mu;
+    std::vector<std::shared_ptr<void>> items;
+  };
+  std::shared_ptr<FitPool> fit_pool = std::make_shared<FitPool>();
 
   gi::MatrixDesc desc() const {
     gi::MatrixDesc d;
