@@ -103,10 +103,10 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   TRY(ws->dalloc(ws->oidx, kcap));
   TRY(ws->dalloc(ws->oval, kcap));
   TRY(ws->dalloc(ws->ocnt, 1));
-  TRY(ws->dalloc(ws->didx, 2 * kcap + 16));
-  TRY(ws->dalloc(ws->dw, 2 * kcap + 16));
+  TRY(ws->dalloc(ws->didx, 4 * (4 * kcap + 16)));
+  TRY(ws->dalloc(ws->dw, 4 * (4 * kcap + 16)));
   GI_CUDA_TRY(cudaMemsetAsync(ws->ticket, 0, sizeof(uint32_t), ws->stream));
-  GI_CUDA_TRY(cudaMallocHost(&ws->hin, sizeof(double) * (size_t)(4 * kcap + 64 + 2 * c)));
+  GI_CUDA_TRY(cudaMallocHost(&ws->hin, sizeof(double) * (size_t)(8 * (4 * kcap + 16) + 64)));
   GI_CUDA_TRY(cudaMallocHost(&ws->hout, sizeof(double) * (size_t)(8 + 2 * c + 4 * kcap + 64)));
   out = ws;
   return 0;
@@ -127,24 +127,30 @@ class NativeFit {
   double aty_ms = 0.0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
-  // upload a sparse vector (idx, w) into didx/dw
-  int upload_sparse(const std::vector<int64_t>& idx, const std::vector<double>& w) {
+  // Upload a sparse vector (idx, w) into the device slot `slot` (0..3).  Each
+  // slot has its own pinned staging region, so several uploads may be in
+  // flight between two syncs without the host overwriting unread bytes.
+  int upload_sparse(const std::vector<int64_t>& idx, const std::vector<double>& w, int slot = 0) {
     const int64_t k = (int64_t)idx.size();
     if (k == 0) return 0;
-    int64_t* hi = reinterpret_cast<int64_t*>(ws_->hin);
-    double* hw = ws_->hin + ws_->kcap * 2 + 16;
+    const int64_t cap = 4 * ws_->kcap + 16;  // per slot: idx | w
+    int64_t* hi = reinterpret_cast<int64_t*>(ws_->hin + slot * 2 * cap);
+    double* hw = ws_->hin + slot * 2 * cap + cap;
     memcpy(hi, idx.data(), sizeof(int64_t) * k);
     memcpy(hw, w.data(), sizeof(double) * k);
-    GI_CUDA_TRY(cudaMemcpyAsync(ws_->didx, hi, sizeof(int64_t) * k, cudaMemcpyHostToDevice,
-                                ws_->stream));
-    GI_CUDA_TRY(cudaMemcpyAsync(ws_->dw, hw, sizeof(double) * k, cudaMemcpyHostToDevice,
-                                ws_->stream));
+    GI_CUDA_TRY(cudaMemcpyAsync(ws_->didx + slot * cap, hi, sizeof(int64_t) * k,
+                                cudaMemcpyHostToDevice, ws_->stream));
+    GI_CUDA_TRY(cudaMemcpyAsync(ws_->dw + slot * cap, hw, sizeof(double) * k,
+                                cudaMemcpyHostToDevice, ws_->stream));
     return 0;
   }
+  int64_t* didx(int slot) { return ws_->didx + slot * (4 * ws_->kcap + 16); }
+  double* dw(int slot) { return ws_->dw + slot * (4 * ws_->kcap + 16); }
 
   int upload_cov(const std::vector<double>& cv) {
     if (ws_->c == 0) return 0;
-    double* hc = ws_->hin + 4 * ws_->kcap + 32;
+    double* hc = ws_->hin + 4 * 2 * (4 * ws_->kcap + 16) + cov_slot_ * 16;
+    cov_slot_ = (cov_slot_ + 1) & 3;
     memcpy(hc, cv.data(), sizeof(double) * ws_->c);
     GI_CUDA_TRY(cudaMemcpyAsync(ws_->cvec, hc, sizeof(double) * ws_->c, cudaMemcpyHostToDevice,
                                 ws_->stream));
@@ -155,6 +161,7 @@ class NativeFit {
     GI_CUDA_TRY(cudaStreamSynchronize(ws_->stream));
     return 0;
   }
+  int cov_slot_ = 0;
 
   // _refresh_state: returns loss, max|g|, g_cov, g on the support
   int refresh(const std::vector<int64_t>& sup, const std::vector<double>& w,
@@ -165,9 +172,8 @@ class NativeFit {
     const bool has_fit = !sup.empty();
     if (has_fit) {
       // the upload buffers are reused below for the gather, so sync the ax inputs first
-      TRY(upload_sparse(sup, w));
-      TRY(gi::launch_ax(d, ws_->u, ws_->v, ws_->didx, ws_->dw, (int64_t)sup.size(), ws_->fitb, 0,
-                        s));
+      TRY(upload_sparse(sup, w, 0));
+      TRY(gi::launch_ax(d, ws_->u, ws_->v, didx(0), dw(0), (int64_t)sup.size(), ws_->fitb, 0, s));
       ++launches;
     }
     TRY(upload_cov(bcov));
@@ -194,8 +200,8 @@ class NativeFit {
     }
     const int64_t ks = (int64_t)sup.size();
     if (ks) {
-      // didx still holds the support (uploaded above, stream-ordered)
-      TRY(gi::launch_gather(ks, ws_->didx, ws_->g, ws_->oval, s));
+      // slot 0 still holds the support (uploaded above, stream-ordered)
+      TRY(gi::launch_gather(ks, didx(0), ws_->g, ws_->oval, s));
       ++launches;
     }
     double* ho = ws_->hout;
@@ -219,13 +225,13 @@ class NativeFit {
     return 0;
   }
 
-  // || X_idx w + C wcov ||^2 over the view's rows
-  int image_sumsq(const std::vector<int64_t>& idx, const std::vector<double>& w,
-                  const std::vector<double>* wcov, double& out) {
+  // || X_idx w + C wcov ||^2 over the view's rows -> scal[4] (enqueue only)
+  int image_enqueue(const std::vector<int64_t>& idx, const std::vector<double>& w,
+                    const std::vector<double>* wcov) {
     const gi::MatrixDesc d = h_->desc();
     cudaStream_t s = ws_->stream;
-    TRY(upload_sparse(idx, w));
-    TRY(gi::launch_ax(d, ws_->u, ws_->v, ws_->didx, ws_->dw, (int64_t)idx.size(), ws_->img, 0, s));
+    TRY(upload_sparse(idx, w, 1));
+    TRY(gi::launch_ax(d, ws_->u, ws_->v, didx(1), dw(1), (int64_t)idx.size(), ws_->img, 0, s));
     ++launches;
     if (wcov && ws_->c) {
       TRY(upload_cov(*wcov));
@@ -238,23 +244,44 @@ class NativeFit {
     }
     TRY(gi::launch_sumsq(ws_->n, ws_->img, ws_->scal, 4, ws_->partials, ws_->ticket, s));
     ++launches;
+    return 0;
+  }
+
+  int image_sumsq(const std::vector<int64_t>& idx, const std::vector<double>& w,
+                  const std::vector<double>* wcov, double& out) {
+    TRY(image_enqueue(idx, w, wcov));
     GI_CUDA_TRY(cudaMemcpyAsync(ws_->hout, ws_->scal + 4, sizeof(double), cudaMemcpyDeviceToHost,
-                                s));
+                                ws_->stream));
     TRY(sync());
     out = ws_->hout[0];
     return 0;
   }
 
   // k largest |g| (mode 0) or |beta - mu g| (mode 1), sorted by index
-  int topk(int mode, double mu, int64_t k, std::vector<Pair>& out) {
+  // `mu_dev` (optional): take mu from the device (scal[5]) and also return
+  // scal[4] (den) and scal[5] (mu) through `den_mu` in the same sync
+  int topk(int mode, double mu, int64_t k, std::vector<Pair>& out, double* den_mu = nullptr) {
     out.clear();
-    if (ws_->p == 0 || k <= 0) return 0;
-    const int64_t ke = std::min(k, ws_->kcap);
     cudaStream_t s = ws_->stream;
+    if (ws_->p == 0 || k <= 0) {
+      if (den_mu) {
+        GI_CUDA_TRY(cudaMemcpyAsync(ws_->hout, ws_->scal + 4, 2 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, s));
+        TRY(sync());
+        den_mu[0] = ws_->hout[0];
+        den_mu[1] = ws_->hout[1];
+      }
+      return 0;
+    }
+    const int64_t ke = std::min(k, ws_->kcap);
     TRY(gi::launch_topk(ws_->p, ke, mode, ws_->beta, ws_->g, mu, 0, ws_->ckey, ws_->cidx,
-                        ws_->cval, ws_->oidx, ws_->oval, nullptr, ws_->ocnt, s));
+                        ws_->cval, ws_->oidx, ws_->oval, nullptr, ws_->ocnt, s,
+                        den_mu ? ws_->scal + 5 : nullptr));
     launches += 2;
     double* ho = ws_->hout;
+    if (den_mu)
+      GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + 2 * ke, ws_->scal + 4, 2 * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
     GI_CUDA_TRY(cudaMemcpyAsync(ho, ws_->ocnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     GI_CUDA_TRY(cudaMemcpyAsync(ho + 1, ws_->oidx, sizeof(int64_t) * ke, cudaMemcpyDeviceToHost, s));
     GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + ke, ws_->oval, sizeof(double) * ke,
@@ -265,16 +292,20 @@ class NativeFit {
     const int64_t* hi = reinterpret_cast<const int64_t*>(ho + 1);
     out.resize((size_t)cnt);
     for (int64_t t = 0; t < cnt; ++t) out[t] = Pair{hi[t], ho[1 + ke + t]};
+    if (den_mu) {
+      den_mu[0] = ho[1 + 2 * ke];
+      den_mu[1] = ho[2 + 2 * ke];
+    }
     std::sort(out.begin(), out.end(), [](const Pair& a, const Pair& b) { return a.idx < b.idx; });
     return 0;
   }
 
   int scatter_beta(const std::vector<int64_t>& idx, const std::vector<double>& w) {
     if (idx.empty()) return 0;
-    TRY(upload_sparse(idx, w));
-    TRY(gi::launch_scatter((int64_t)idx.size(), ws_->didx, ws_->dw, ws_->beta, ws_->stream));
+    TRY(upload_sparse(idx, w, 2));
+    TRY(gi::launch_scatter((int64_t)idx.size(), didx(2), dw(2), ws_->beta, ws_->stream));
     ++launches;
-    return sync();  // the upload staging is reused by the next phase
+    return 0;  // slot 2's staging is not touched again before the refresh's sync
   }
 
  private:
@@ -452,17 +483,23 @@ extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
           gi_set_error("gradient vanishes on the restriction; nothing to step on");
           return -2;
         }
-        double den = 0.0;
-        TRY(F.image_sumsq(ridx, rg, c ? &gcov : nullptr, den));
+        // den = ||X_S g_S + C g_cov||^2 and mu = num / den stay on the device; the
+        // first candidate top-k reads mu there, so den, mu and the candidate come
+        // back in one sync (iht.py:276-280)
+        TRY(F.image_enqueue(ridx, rg, c ? &gcov : nullptr));
+        TRY(gi::launch_ratio(num, ws->scal, 4, 5, ws->stream));
+        double den_mu[2] = {0.0, 0.0};
+        TRY(F.topk(1, 0.0, cfg->k, cand, den_mu));
+        const double den = den_mu[0];
         if (den == 0.0 || !std::isfinite(den)) {
           gi_set_error("degenerate active set: restricted columns have zero image");
           return -3;
         }
-        double mu = num / den;
+        double mu = den_mu[1];  // == num / den, computed on the device in IEEE fp64
         bool accepted = false;
         int64_t bt = 0;
         for (int64_t tries = 0; tries <= cfg->max_backtracks; ++tries) {
-          TRY(F.topk(1, mu, cfg->k, cand));
+          if (tries > 0) TRY(F.topk(1, mu, cfg->k, cand));
           new_sup.clear();
           new_w.clear();
           for (const Pair& q : cand)
@@ -525,10 +562,24 @@ extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
         step_inf = 0.0;
         for (double x : dval) step_inf = std::max(step_inf, std::fabs(x));
         for (double x : dcov) step_inf = std::max(step_inf, std::fabs(x));
-        // beta <- candidate; refresh (iht.py:311-321)
-        std::vector<double> zeros(sup.size(), 0.0);
-        TRY(F.scatter_beta(sup, zeros));
-        TRY(F.scatter_beta(new_sup, new_w));
+        // beta <- candidate (old-only entries to 0, new entries to their values; one
+        // upload), then refresh (iht.py:311-321)
+        {
+          std::vector<int64_t> uidx;
+          std::vector<double> uval;
+          size_t a2 = 0, b2 = 0;
+          while (a2 < sup.size() || b2 < new_sup.size()) {
+            if (b2 >= new_sup.size() || (a2 < sup.size() && sup[a2] < new_sup[b2])) {
+              uidx.push_back(sup[a2++]);
+              uval.push_back(0.0);
+            } else {
+              if (a2 < sup.size() && sup[a2] == new_sup[b2]) ++a2;
+              uidx.push_back(new_sup[b2]);
+              uval.push_back(new_w[b2++]);
+            }
+          }
+          TRY(F.scatter_beta(uidx, uval));
+        }
         sup = new_sup;
         w = new_w;
         bcov = cand_cov;

@@ -403,10 +403,12 @@ __device__ __forceinline__ uint64_t key_of(double val) {
 // (cand_key = 0 marks an unused slot).
 __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(
     int64_t p, int64_t k, int mode, const double* __restrict__ beta,
-    const double* __restrict__ g, double mu, int64_t idx_base, uint64_t* __restrict__ cand_key,
+    const double* __restrict__ g, double mu_host, const double* __restrict__ mu_dev,
+    int64_t idx_base, uint64_t* __restrict__ cand_key,
     int64_t* __restrict__ cand_idx, double* __restrict__ cand_val) {
   __shared__ uint64_t keys[kTopkChunk];
   __shared__ unsigned int s_pos;
+  const double mu = mu_dev ? *mu_dev : mu_host;
   const int64_t lo = (int64_t)blockIdx.x * kTopkChunk;
   const int64_t hi = lo + kTopkChunk < p ? lo + kTopkChunk : p;
   const int64_t m = hi - lo;
@@ -488,17 +490,29 @@ int64_t topk_blocks(int64_t p) { return (p + kTopkChunk - 1) / kTopkChunk; }
 int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double* g, double mu,
                 int64_t idx_base, uint64_t* cand_key, int64_t* cand_idx, double* cand_val,
                 int64_t* out_idx, double* out_val, uint64_t* out_key, int64_t* out_count,
-                cudaStream_t s) {
+                cudaStream_t s, const double* mu_dev) {
   if (k <= 0 || p <= 0) {
     GI_CUDA_TRY(cudaMemsetAsync(out_count, 0, sizeof(int64_t), s));
     return 0;
   }
   const int64_t nb = topk_blocks(p);
-  topk_local_kernel<<<(unsigned)nb, kTopkThreads, 0, s>>>(p, k, mode, beta, g, mu, idx_base,
+  topk_local_kernel<<<(unsigned)nb, kTopkThreads, 0, s>>>(p, k, mode, beta, g, mu, mu_dev,
+                                                          idx_base,
                                                           cand_key, cand_idx, cand_val);
   GI_LAUNCH_CHECK();
   topk_merge_kernel<<<1, 1024, 0, s>>>(nb * k, k, cand_key, cand_idx, cand_val, out_idx,
                                        out_val, out_key, out_count);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+// scal[out] = num / scal[den]  (the normalised step on the device, iht.py:244)
+__global__ void ratio_kernel(double num, double* scal, int den, int out) {
+  scal[out] = num / scal[den];
+}
+
+int launch_ratio(double num, double* scal, int den, int out, cudaStream_t s) {
+  ratio_kernel<<<1, 1, 0, s>>>(num, scal, den, out);
   GI_LAUNCH_CHECK();
   return 0;
 }
