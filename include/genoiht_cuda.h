@@ -51,6 +51,13 @@ int gi_device_sync(int device);
  * _packed_stats (:239-246): uploads `data` (host, variant-major p x ceil(n/4),
  * kept verbatim) to `device` and computes u, v bit-identically. */
 int gi_matrix_from_bed(const uint8_t *data, int64_t n, int64_t p, int device, gi_matrix **out);
+/* Streaming construction (a BED file larger than host RAM, or one SNP shard of
+ * it): create an empty n x p matrix, upload variant-major rows [j0, j0+count)
+ * in any number of calls (host buffer count x ceil(n/4), staged through pinned
+ * memory), then compute the statistics once.  read_bed (plink_io.py:82-100). */
+int gi_matrix_create(int64_t n, int64_t p, int device, gi_matrix **out);
+int gi_matrix_upload_bed(gi_matrix *h, int64_t j0, int64_t count, const uint8_t *data);
+int gi_matrix_finalize(gi_matrix *h);
 /* Device-side synthetic genotypes with the law of random_packed_matrix
  * (simulate.py:56-65) from a counter-based stream; SNP j_base + j of the
  * unsharded matrix gets identical bytes in any shard.  CPU twin: oracle/. */

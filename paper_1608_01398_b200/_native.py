@@ -55,6 +55,9 @@ def _declare(lib):
         "gi_device_info": ([c_int, P, P, P], c_int),
         "gi_device_sync": ([c_int], c_int),
         "gi_matrix_from_bed": ([P, c_i64, c_i64, c_int, P], c_int),
+        "gi_matrix_create": ([c_i64, c_i64, c_int, P], c_int),
+        "gi_matrix_upload_bed": ([P, c_i64, c_i64, P], c_int),
+        "gi_matrix_finalize": ([P], c_int),
         "gi_matrix_synth": ([c_u64, c_i64, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_int, P], c_int),
         "gi_matrix_with_stats": ([P, P, P, P], c_int),
         "gi_matrix_subset_rows": ([P, P, c_i64, P], c_int),

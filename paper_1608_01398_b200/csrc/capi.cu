@@ -91,42 +91,62 @@ int gi_device_sync(int device) {
   return 0;
 }
 
-int gi_matrix_from_bed(const uint8_t* data, int64_t n, int64_t p, int device, gi_matrix** out) {
+int gi_matrix_create(int64_t n, int64_t p, int device, gi_matrix** out) {
   std::unique_ptr<gi_matrix> h;
   TRY(matrix_shell(n, p, device, out, h));
-  DeviceGuard g(device);
-  if (p > 0 && h->nb > 0) {
-    CHECK_ARG(data != nullptr, "BED buffer is NULL");
-    // stream the upload in chunks of ~256 MiB through a pinned staging buffer
-    const int64_t chunk = std::max<int64_t>(1, (int64_t)(256ll << 20) / h->nb);
-    const int64_t cmax = std::min(chunk, p);
-    std::shared_ptr<DevMem> dbuf;
-    TRY(alloc(dbuf, (size_t)(cmax * h->nb), device, false));
-    void* pinned = nullptr;
-    GI_CUDA_TRY(cudaMallocHost(&pinned, (size_t)(cmax * h->nb)));
-    int rc = 0;
-    gi::MatrixDesc d = h->desc();
-    for (int64_t j0 = 0; j0 < p && rc == 0; j0 += cmax) {
-      const int64_t cnt = std::min(cmax, p - j0);
-      memcpy(pinned, data + j0 * h->nb, (size_t)(cnt * h->nb));
-      if (cudaMemcpyAsync(dbuf->ptr, pinned, (size_t)(cnt * h->nb), cudaMemcpyHostToDevice,
-                          h->stream) != cudaSuccess) {
-        gi_set_error("H2D copy of the BED buffer failed");
-        rc = -1;
-        break;
-      }
-      rc = gi::launch_upload_tiles(d, static_cast<uint8_t*>(h->x->ptr),
-                                   static_cast<const uint8_t*>(dbuf->ptr), j0, cnt, h->stream);
-      if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
-        gi_set_error("upload failed");
-        rc = -1;
-      }
-    }
-    cudaFreeHost(pinned);
-    if (rc) return -1;
-  }
-  TRY(finish_stats(h.get()));
   *out = h.release();
+  return 0;
+}
+
+int gi_matrix_upload_bed(gi_matrix* h, int64_t j0, int64_t count, const uint8_t* data) {
+  CHECK_ARG(h != nullptr, "NULL handle");
+  CHECK_ARG(j0 >= 0 && count >= 0 && j0 + count <= h->p, "SNP range out of bounds");
+  if (count == 0 || h->nb == 0) return 0;
+  CHECK_ARG(data != nullptr, "BED buffer is NULL");
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard g(h->device);
+  // stream through a pinned staging buffer in chunks of ~256 MiB
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>((int64_t)(256ll << 20) / h->nb,
+                                                               count));
+  TRY(h->s_a.ensure((size_t)(chunk * h->nb), h->device));
+  void* pinned = nullptr;
+  GI_CUDA_TRY(cudaMallocHost(&pinned, (size_t)(chunk * h->nb)));
+  int rc = 0;
+  const gi::MatrixDesc d = h->desc();
+  for (int64_t c0 = 0; c0 < count && rc == 0; c0 += chunk) {
+    const int64_t cnt = std::min(chunk, count - c0);
+    memcpy(pinned, data + c0 * h->nb, (size_t)(cnt * h->nb));
+    if (cudaMemcpyAsync(h->s_a.mem->ptr, pinned, (size_t)(cnt * h->nb), cudaMemcpyHostToDevice,
+                        h->stream) != cudaSuccess) {
+      gi_set_error("H2D copy of the BED buffer failed");
+      rc = -1;
+      break;
+    }
+    rc = gi::launch_upload_tiles(d, static_cast<uint8_t*>(h->x->ptr), h->s_a.as<uint8_t>(),
+                                 j0 + c0, cnt, h->stream);
+    if (rc == 0 && cudaStreamSynchronize(h->stream) != cudaSuccess) {
+      gi_set_error("BED upload failed");
+      rc = -1;
+    }
+  }
+  cudaFreeHost(pinned);
+  return rc;
+}
+
+int gi_matrix_finalize(gi_matrix* h) {
+  CHECK_ARG(h != nullptr, "NULL handle");
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard g(h->device);
+  return finish_stats(h);
+}
+
+int gi_matrix_from_bed(const uint8_t* data, int64_t n, int64_t p, int device, gi_matrix** out) {
+  gi_matrix* h = nullptr;
+  TRY(gi_matrix_create(n, p, device, &h));
+  std::unique_ptr<gi_matrix> guard(h);
+  TRY(gi_matrix_upload_bed(h, 0, p, data));
+  TRY(gi_matrix_finalize(h));
+  *out = guard.release();
   return 0;
 }
 

@@ -148,3 +148,19 @@ def test_cv_errors():
     plan2 = gi.CvPlan.build(30, 3, np.array([1, 2]), seed=2)
     with pytest.raises(RuntimeError, match=r"fold \d, k=1"):
         gi.cv_iht(view, y, plan2, gi.IhtConfig(k=2))
+
+
+def test_cli_bench_tables(tmp_path):
+    from paper_1608_01398_b200.__main__ import main
+    out = str(tmp_path / "b")
+    assert main(["bench", "--synthetic", "400,800", "--path", "2:10:2", "--mode", "gpu,gpu+seq",
+                 "--repetitions", "2", "--out", out, "--seed", "13"]) == 0
+    lines = open(out + ".bench.tsv").read().splitlines()
+    assert lines[0].startswith("# genoiht=") and "command=bench" in lines[0]
+    assert lines[1].split("\t") == ["mode", "repetitions", "mean_seconds", "sd_seconds",
+                                    "rel_to_dense"]
+    models = [ln.split("\t") for ln in open(out + ".bench_models.tsv").read().splitlines()[2:]]
+    by_mode = {}
+    for mode, k, support in models:
+        by_mode.setdefault(mode, []).append((k, support))
+    assert by_mode["gpu"] == by_mode["gpu+seq"]  # concurrent path == sequential loop
