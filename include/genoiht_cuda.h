@@ -132,7 +132,7 @@ int gi_dev_residual(int64_t n, const double *d_y, const double *d_fit, const dou
 int gi_dev_center(int64_t n, int64_t n_pad, const double *d_r, const uint8_t *d_keep,
                   double *d_scal, float *d_rt, double *d_partials, uint32_t *d_ticket,
                   void *stream);
-/* d_gcov[l] = -sum_i C[i, l] r_i, l < c <= 8 */
+/* d_gcov[l] = -sum_i C[i, l] r_i, l < c */
 int gi_dev_covgrad(int64_t n, const double *d_C, int64_t c, const double *d_r, double *d_gcov,
                    double *d_partials, uint32_t *d_ticket, void *stream);
 /* d_scal[slot] = max |x| */
@@ -193,7 +193,7 @@ typedef struct {
 
 /* Replaces genoiht.fit (iht.py:326-354) on one GPU: the complete IHT loop with
  * device kernels, one host sync per phase.  y (n) and C (row-major n x c,
- * c <= 8) are host arrays over the handle's n samples; keep (n, optional)
+ * c <= 64) are host arrays over the handle's n samples; keep (n, optional)
  * restricts the fit to rows with keep != 0 (cross-validation training rows:
  * other rows' residuals are pinned to 0); u, v (p, optional) override the
  * handle's stats; warm_idx/warm_w (warm_k, sorted, may be NULL) seed the

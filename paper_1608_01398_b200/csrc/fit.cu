@@ -106,7 +106,7 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   TRY(ws->dalloc(ws->didx, 4 * (4 * kcap + 16)));
   TRY(ws->dalloc(ws->dw, 4 * (4 * kcap + 16)));
   GI_CUDA_TRY(cudaMemsetAsync(ws->ticket, 0, sizeof(uint32_t), ws->stream));
-  GI_CUDA_TRY(cudaMallocHost(&ws->hin, sizeof(double) * (size_t)(8 * (4 * kcap + 16) + 64)));
+  GI_CUDA_TRY(cudaMallocHost(&ws->hin, sizeof(double) * (size_t)(8 * (4 * kcap + 16) + 4 * 64)));
   GI_CUDA_TRY(cudaMallocHost(&ws->hout, sizeof(double) * (size_t)(8 + 2 * c + 4 * kcap + 64)));
   out = ws;
   return 0;
@@ -149,7 +149,7 @@ class NativeFit {
 
   int upload_cov(const std::vector<double>& cv) {
     if (ws_->c == 0) return 0;
-    double* hc = ws_->hin + 4 * 2 * (4 * ws_->kcap + 16) + cov_slot_ * 16;
+    double* hc = ws_->hin + 4 * 2 * (4 * ws_->kcap + 16) + cov_slot_ * 64;
     cov_slot_ = (cov_slot_ + 1) & 3;
     memcpy(hc, cv.data(), sizeof(double) * ws_->c);
     GI_CUDA_TRY(cudaMemcpyAsync(ws_->cvec, hc, sizeof(double) * ws_->c, cudaMemcpyHostToDevice,
@@ -335,7 +335,7 @@ extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
                       const gi_fit_config* cfg, const int64_t* warm_idx, const double* warm_w,
                       int64_t warm_k, const double* bcov0, gi_fit_result* res) {
   CHECK_ARG(h && cfg && res, "NULL argument");
-  CHECK_ARG(c >= 0 && c <= 8, "the native loop supports at most 8 covariate columns");
+  CHECK_ARG(c >= 0 && c <= 64, "the native loop supports at most 64 covariate columns");
   CHECK_ARG(c == 0 || C != nullptr, "covariate matrix is NULL");
   CHECK_ARG(cfg->k >= 0 && cfg->max_iter >= 1, "invalid solver configuration");
   CHECK_ARG(res->trace_cap >= cfg->max_iter + 1, "loss trace buffer is too small");

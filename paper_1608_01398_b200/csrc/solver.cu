@@ -151,7 +151,7 @@ __global__ void center_kernel(int64_t n, int64_t n_pad, const double* __restrict
 }
 
 // gcov[l] = -sum_i C[i, l] r_i  (covariate block of the gradient)
-__global__ void covgrad_kernel(int64_t n, const double* __restrict__ C, int c,
+__global__ void covgrad_kernel(int64_t n, const double* __restrict__ C, int stride, int c,
                                const double* __restrict__ r, double* __restrict__ gcov,
                                RedWs ws) {
   __shared__ double sh[8 * 32];
@@ -163,7 +163,7 @@ __global__ void covgrad_kernel(int64_t n, const double* __restrict__ C, int c,
     const double ri = r[i];
 #pragma unroll
     for (int l = 0; l < 8; ++l)
-      if (l < c) acc[l] += C[i * c + l] * ri;
+      if (l < c) acc[l] += C[i * stride + l] * ri;
   }
   block_sum<8>(acc, sh);
   if (threadIdx.x == 0)
@@ -259,13 +259,14 @@ int launch_center(int64_t n, int64_t n_pad, const double* r, const uint8_t* keep
 int launch_covgrad(int64_t n, const double* C, int c, const double* r, double* gcov,
                    double* partials, unsigned int* ticket, cudaStream_t s) {
   if (c <= 0) return 0;
-  if (c > 8) {
-    gi_set_error("at most 8 covariate columns are supported on the device path");
-    return -1;
-  }
   RedWs ws{partials, ticket};
-  covgrad_kernel<<<red_grid(n), kRedThreads, 0, s>>>(n, C, c, r, gcov, ws);
-  GI_LAUNCH_CHECK();
+  // 8 columns per launch; column block l0 reads C[i * c + l0 + l] through a
+  // row stride of c
+  for (int l0 = 0; l0 < c; l0 += 8) {
+    const int cc = c - l0 < 8 ? c - l0 : 8;
+    covgrad_kernel<<<red_grid(n), kRedThreads, 0, s>>>(n, C + l0, c, cc, r, gcov + l0, ws);
+    GI_LAUNCH_CHECK();
+  }
   return 0;
 }
 

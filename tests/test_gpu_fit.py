@@ -164,3 +164,22 @@ def test_cli_bench_tables(tmp_path):
     for mode, k, support in models:
         by_mode.setdefault(mode, []).append((k, support))
     assert by_mode["gpu"] == by_mode["gpu+seq"]  # concurrent path == sequential loop
+
+
+@pytest.mark.parametrize("native", [True, False], ids=["native-loop", "python-loop"])
+def test_many_covariates_and_budget_above_p(native):
+    gi = _gi()
+    rng = np.random.default_rng(21)
+    n, p = 300, 20
+    codes = oracle.random_codes(n, p, seed=21, missing_rate=0.05)
+    covar = rng.standard_normal((n, 11))  # 12 covariate columns with the intercept
+    block = gi.CovariateBlock.build(covar, n=n)
+    view = gi.StandardizedView(gi.PackedGenotypeMatrix.from_codes(codes), block)
+    ref = oracle.OracleView(oracle.OraclePacked.from_codes(codes), block.values)
+    y = ref.geno.ax_columns(np.array([2, 7]), np.array([1.0, -0.5])) + covar[:, 3] \
+        + rng.normal(0, 0.3, n)
+    for k in (5, 30):  # k > p keeps every column (iht.py:42-43)
+        want = oracle.fit(ref, y, k)
+        got = gi.fit(view, y, gi.IhtConfig(k=k), native=native)
+        _assert_fit(got, want.support, want.weights, want.covar, want.loss_trace,
+                    want.iterations, want.reason)

@@ -54,7 +54,7 @@ def main():
     t1 = time.time()
     got = gi.fit(view, y, gi.IhtConfig(k=a.k))
     t2 = time.time()
-    data = np.array(m.data)  # verbatim BED bytes, p x ceil(n/4)
+    data = np.asarray(m.data)  # verbatim BED bytes, p x ceil(n/4) (no second copy)
     ref = oracle.OraclePacked.from_bed(data, a.n)
     assert np.array_equal(ref.u, m.u) and np.array_equal(ref.v, m.v), "stats differ"
     oracle.set_threads(os.cpu_count() or 1)
