@@ -13,7 +13,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgenoiht_cuda.so")
+LIB_PATH = os.environ.get("GI_LIB_PATH") or os.path.join(_HERE, "libgenoiht_cuda.so")
 
 _lib = None
 _lock = threading.Lock()

@@ -105,7 +105,7 @@ struct FastArgs {
   double scale;
   double* out;
   int64_t n_items;
-  int flags;  // experiment knobs: 1 = skip lookups, 2 = L2 prefetch ahead
+  unsigned long long* gmax;  // optional: atomicMax of |out_j| (bits of a non-negative double)
 };
 
 __device__ __forceinline__ float dose_term(int code, float r) {
@@ -131,9 +131,10 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 
-// Table build: all 256 threads.  Thread (w = lane, k = byte within word,
-// half) writes 128 entries T[pos = 4w + k][b] for b in [128 half, 128 half + 128)
-// at shared byte address  tbl + (k >> 1) * 65536 + b * 256 + (k & 1) * 128 + 4 w,
+// Table build: all 384 threads.  Thread (w = lane, k = byte within word,
+// third) writes the entries T[pos = 4w + k][b] whose high nibble b >> 4 falls in
+// its third of [0, 16) (6, 5 and 5 nibbles) at shared byte address
+//   tbl + (k >> 1) * 65536 + b * 256 + (k & 1) * 128 + 4 w,
 // from the four residuals of samples 16w + 4k .. +3 of the tile.
 __device__ __forceinline__ float4 load_tile_r(const float* __restrict__ rt, int64_t t, int tid) {
   const int w = tid & 31;
@@ -144,17 +145,21 @@ __device__ __forceinline__ float4 load_tile_r(const float* __restrict__ rt, int6
 __device__ __forceinline__ void build_table(uint32_t tbl, float4 r, int tid) {
   const int w = tid & 31;
   const int k = (tid >> 5) & 3;
-  const int half = tid >> 7;
+  const int third = tid >> 7;
+  const int hi0 = third == 0 ? 0 : (third == 1 ? 6 : 11);
+  const int hi1 = third == 0 ? 6 : (third == 1 ? 11 : 16);
   float lo[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c) lo[c] = dose_term(c & 3, r.x) + dose_term(c >> 2, r.y);
   const uint32_t base = tbl + (k >> 1) * 65536 + (k & 1) * 128 + 4 * w;
 #pragma unroll
-  for (int hh = 0; hh < 8; ++hh) {
-    const int hi = half * 8 + hh;
-    const float hv = dose_term(hi & 3, r.z) + dose_term(hi >> 2, r.w);
+  for (int hh = 0; hh < 6; ++hh) {
+    const int hi = hi0 + hh;
+    if (hi < hi1) {
+      const float hv = dose_term(hi & 3, r.z) + dose_term(hi >> 2, r.w);
 #pragma unroll
-    for (int c = 0; c < 16; ++c) sts_f32(base + (hi * 16 + c) * 256, lo[c] + hv);
+      for (int c = 0; c < 16; ++c) sts_f32(base + (hi * 16 + c) * 256, lo[c] + hv);
+    }
   }
 }
 
@@ -297,7 +302,6 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
 
     // copy issuer: lane 0 keeps kSlots blocks of this warp's stream in flight
     BlockCursor issue{(uint32_t)warp, (uint32_t)warp, ng, 0, m.T};
-    BlockCursor pf{(uint32_t)warp, (uint32_t)warp, ng, 0, m.T};
     int next_slot = 0;
     auto issue_one = [&]() {
       if (issue.valid()) {
@@ -313,14 +317,6 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
       next_slot = next_slot + 1 == kSlots ? 0 : next_slot + 1;
     };
     if (has_work) {
-      if (a.flags & 2) {
-        for (int i = 0; i < 8; ++i) {
-          if (pf.valid() && lane == 0)
-            prefetch_l2(xitem + pf.t * tile_stride + (int64_t)pf.gl * GI_BLOCK_BYTES,
-                        GI_BLOCK_BYTES);
-          if (pf.valid()) pf.next();
-        }
-      }
 #pragma unroll
       for (int s2 = 0; s2 < kSlots; ++s2) issue_one();
     }
@@ -328,14 +324,11 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
 
     for (uint32_t gl = warp; gl < ng; gl += kWarps) acc[gl * 32 + lane] = 0.0;
     for (uint32_t gl = tid; gl < ng; gl += kThreads) gflag[gl] = a.group_missing[g0 + gl];
-    const bool builder = tid < 256;
-    float4 r_next = builder ? load_tile_r(a.rt, 0, tid) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 r_next = load_tile_r(a.rt, 0, tid);
     for (int64_t t = 0; t < m.T; ++t) {
       __syncthreads();  // previous tile's lookups are done
-      if (builder) {
-        build_table(tbl, r_next, tid);
-        if (t + 1 < m.T) r_next = load_tile_r(a.rt, t + 1, tid);  // hidden behind the tile
-      }
+      build_table(tbl, r_next, tid);
+      if (t + 1 < m.T) r_next = load_tile_r(a.rt, t + 1, tid);  // hidden behind the tile
       __syncthreads();
       for (uint32_t gl = warp; gl < ng; gl += kWarps) {
         // wait for this slot's next phase (strictly in order: never ambiguous)
@@ -356,18 +349,10 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         __syncwarp();
         next_slot = cur_slot;
         issue_one();  // refill the slot just drained
-        if ((a.flags & 2) && pf.valid()) {
-          if (lane == 0)
-            prefetch_l2(xitem + pf.t * tile_stride + (int64_t)pf.gl * GI_BLOCK_BYTES,
-                        GI_BLOCK_BYTES);
-          pf.next();
-        }
         cur_slot = cur_slot + 1 == kSlots ? 0 : cur_slot + 1;
         float tt = 0.f, tm = 0.f;
         const bool miss = gflag[gl] != 0;
-        if (a.flags & 1)
-          tt = __uint_as_float(wd[0] & 0x3f800000u);
-        else if (miss)
+        if (miss)
           process_group<true>(wd, xb, tt, tm);
         else
           process_group<false>(wd, xb, tt, tm);
@@ -385,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
     // up to rounding when u_j is the mean over the same rows; not for
     // caller-supplied stats such as with_stats / global-standardised folds)
     const double mean = a.scal[1], srt = a.scal[2];
+    double local_max = 0.0;
     for (uint32_t gl = warp; gl < ng; gl += kWarps) {
       const int64_t j = (g0 + gl) * 32 + lane;
       if (j < m.p) {
@@ -392,25 +378,30 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         const double off = (double)a.s1cnt[2 * j] - uj * (double)a.s1cnt[2 * j + 1];
         const double val = a.v[j] * ((acc[gl * 32 + lane] - uj * srt) + mean * off);
         a.out[j] = a.scale * val;
+        local_max = fmax(local_max, fabs(val));
       }
+    }
+    if (a.gmax) {
+      // max|g| for the IHT step (iht.py:257-261): exact and order-independent
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        local_max = fmax(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+      if (lane == 0)
+        atomicMax(a.gmax, (unsigned long long)__double_as_longlong(local_max));
     }
     __syncthreads();  // accumulators, flags and table are reused by the next item
   }
 }
 
-int g_aty_flags = 0;  // experiment knobs (GI_ATY_FLAGS)
-
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
                     const double* u, const double* v, const int32_t* s1cnt,
                     const double* d_scal, double scale, double* out, int num_sms,
-                    cudaStream_t s) {
+                    cudaStream_t s, double* d_gmax) {
   if (m.p == 0) return 0;
 
   static std::once_flag once;
   static cudaError_t cfg_err = cudaSuccess;
   std::call_once(once, [] {
-    const char* env = getenv("GI_ATY_FLAGS");
-    if (env) g_aty_flags = atoi(env);
     cfg_err = cudaFuncSetAttribute(aty_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kSmemFast);
   });
@@ -425,7 +416,7 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
   a.scal = d_scal;
   a.scale = scale;
   a.out = out;
-  a.flags = g_aty_flags;
+  a.gmax = reinterpret_cast<unsigned long long*>(d_gmax);
   const int64_t per_wave = (int64_t)num_sms * kMaxGroups;
   int64_t items = (int64_t)num_sms * ((m.G + per_wave - 1) / per_wave);
   if (items > m.G) items = m.G;

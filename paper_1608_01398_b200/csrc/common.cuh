@@ -116,7 +116,7 @@ int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
                     const double* u, const double* v, const int32_t* s1cnt,
                     const double* d_scal, double scale, double* out, int num_sms,
-                    cudaStream_t s);
+                    cudaStream_t s, double* d_gmax = nullptr);
 int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u,
                      const double* v, const double* d_sum_r, double scale, double* out,
                      cudaStream_t s);

@@ -187,11 +187,11 @@ class NativeFit {
     if (ws_->p) {
       if (ev0) GI_CUDA_TRY(cudaEventRecord(ev0, s));
       TRY(gi::launch_aty_fast(d, static_cast<const uint8_t*>(h_->gmiss->ptr), ws_->rt, ws_->u,
-                              ws_->v, ws_->s1cnt, ws_->scal, -1.0, ws_->g, h_->sms, s));
+                              ws_->v, ws_->s1cnt, ws_->scal, -1.0, ws_->g, h_->sms, s,
+                              ws_->scal + 3));  // max|g| fused into the epilogue
       if (ev1) GI_CUDA_TRY(cudaEventRecord(ev1, s));
       ++aty_launches;
-      TRY(gi::launch_maxabs(ws_->p, ws_->g, ws_->scal, 3, ws_->partials, ws_->ticket, s));
-      launches += 2;
+      ++launches;
     }
     if (ws_->c) {
       TRY(gi::launch_covgrad(ws_->n, ws_->C, (int)ws_->c, ws_->r, ws_->cvec + ws_->c,

@@ -145,6 +145,7 @@ __global__ void center_kernel(int64_t n, int64_t n_pad, const double* __restrict
     const double s = fold_sum(ws.partials, 1, 0, gridDim.x);
     if (threadIdx.x == 0) {
       scal[2] = s;
+      scal[3] = 0.0;  // max|g| accumulator of the X^T r epilogue that follows
       *ws.ticket = 0u;
     }
   }
