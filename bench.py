@@ -56,8 +56,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=100_000)
-    ap.add_argument("--p", type=int, default=1_000_000)
+    ap.add_argument("--samples", dest="n", type=int, default=100_000)
+    ap.add_argument("--snps", dest="p", type=int, default=1_000_000)
     ap.add_argument("--k", type=int, default=20)
     ap.add_argument("--missing", type=float, default=0.0)
     ap.add_argument("--seed", type=int, default=1608)
@@ -331,13 +331,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GI_DIST_BACKEND=gloo lets several ranks share one GPU (host-staged
+    # collectives; used to test the sharded path where only one GPU exists)
+    backend = os.environ.get("GI_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     import paper_1608_01398_b200 as gi
     from paper_1608_01398_b200 import dist as gdist
     from paper_1608_01398_b200.simulate import SimulationSpec, simulate_phenotype
 
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            torch.distributed.init_process_group(backend)
         comm = gdist.TorchComm()
         geno = gdist.ShardedGenotypes.synthetic(a.n, a.p, a.seed, comm, device=local,
                                                 missing_rate=a.missing)

@@ -145,13 +145,17 @@ class ShardEngine:
         k_eff = min(int(k), self.kmax)
         keys, idx, vals = self._topk_local(mode, mu, k_eff)
         if self.comm.world > 1:
-            pad_k = np.zeros(k_eff, np.uint64)
-            pad_i = np.full(k_eff, -1, np.int64)
-            pad_v = np.zeros(k_eff)
-            pad_k[: keys.size], pad_i[: idx.size], pad_v[: vals.size] = keys, idx, vals
-            keys = np.concatenate(self.comm.allgather_host(pad_k.view(np.int64))).view(np.uint64)
-            idx = np.concatenate(self.comm.allgather_host(pad_i))
-            vals = np.concatenate(self.comm.allgather_host(pad_v))
+            # one all-gather of (key bits | index | value) per rank, 8 bytes each
+            packed = np.zeros((3, k_eff), np.int64)
+            packed[1] = -1
+            packed[0, : keys.size] = keys.view(np.int64)
+            packed[1, : idx.size] = idx
+            packed[2, : vals.size] = np.asarray(vals, np.float64).view(np.int64)
+            parts = self.comm.allgather_host(packed.reshape(-1))
+            stacked = np.stack([p_.reshape(3, k_eff) for p_ in parts], axis=0)
+            keys = stacked[:, 0].reshape(-1).view(np.uint64)
+            idx = stacked[:, 1].reshape(-1)
+            vals = np.ascontiguousarray(stacked[:, 2].reshape(-1)).view(np.float64)
         return merge_topk(keys, idx, vals, k_eff)
 
 
