@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
     const uint32_t ng = (uint32_t)(g1 - g0);
     const uint8_t* xitem = m.x + block_offset(0, g0, m.G);
     const bool has_work = (uint32_t)warp < ng;
+    GI_ASSERT(ng <= (uint32_t)kMaxGroups && g1 <= m.G);
 
     // copy issuer: lane 0 keeps kSlots blocks of this warp's stream in flight
     BlockCursor issue{(uint32_t)warp, (uint32_t)warp, ng, 0, m.T};
@@ -308,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         if (lane == 0) {
           const uint32_t bar = bar0 + 8 * next_slot;
           mbar_expect_tx(bar, GI_BLOCK_BYTES);
+          GI_ASSERT(issue.t < m.T && issue.gl < ng);
           bulk_g2s(slot_addr[next_slot],
                    xitem + issue.t * tile_stride + (int64_t)issue.gl * GI_BLOCK_BYTES,
                    GI_BLOCK_BYTES, bar);
@@ -337,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         for (int s2 = 0; s2 < kSlots; ++s2)
           if (s2 == cur_slot) u0 = uses[s2];
         mbar_wait(bar0 + 8 * cur_slot, u0 & 1);
+        GI_ASSERT(gl < ng && t < m.T);
         uint32_t wd[32];
         uint32_t sa = 0;
 #pragma unroll

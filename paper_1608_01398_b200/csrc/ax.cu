@@ -26,6 +26,7 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
   __shared__ int live[kAxMaxCols];
   for (int t = threadIdx.x; t < k; t += blockDim.x) {
     const int64_t j = idx[t];
+    GI_ASSERT(j >= 0 && j < m.p);
     const double scale = __dmul_rn(w[t], v[j]);
     const double shift = __dmul_rn(u[j], scale);
     cols[t] = j;
@@ -55,7 +56,7 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
         const int t = t0 + b;
         words[b] = (t < k && live[t])
                        ? __ldg(reinterpret_cast<const uint32_t*>(
-                             m.x + word_offset(tile, cols[t], wp, m.G)))
+                             m.x + word_offset_chk(m, tile, cols[t], wp)))
                        : 0u;
       }
 #pragma unroll
@@ -105,9 +106,10 @@ __global__ void decompress_kernel(MatrixDesc m, const double* __restrict__ u,
     const int64_t t = e / words;
     const int64_t wg = e - t * words;
     const int64_t j = idx[t];
+    GI_ASSERT(j >= 0 && j < m.p);
     const double uj = u[j], vj = v[j];
     const uint32_t word =
-        *reinterpret_cast<const uint32_t*>(m.x + word_offset(wg >> 5, j, (int)(wg & 31), m.G));
+        *reinterpret_cast<const uint32_t*>(m.x + word_offset_chk(m, wg >> 5, j, (int)(wg & 31)));
     const int64_t i0 = wg * 16;
     double* row = out_t + t * m.n;
 #pragma unroll

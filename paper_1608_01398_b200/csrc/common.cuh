@@ -15,6 +15,24 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+
+// Device-side bounds checks, compiled in with -DGI_DEBUG (make DEBUG=1 builds
+// libgenoiht_cuda_debug.so; tests run against it with GI_LIB_PATH).  A failed
+// check prints the condition and traps, which surfaces as a CUDA error.
+#ifdef GI_DEBUG
+#define GI_ASSERT(cond)                                                         \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      printf("GI_ASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+      __trap();                                                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define GI_ASSERT(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 #define GI_TILE_SAMPLES 512
 #define GI_TILE_BYTES 128
@@ -35,6 +53,13 @@ struct MatrixDesc {
 
 __host__ __device__ inline int64_t block_offset(int64_t t, int64_t g, int64_t G) {
   return (t * G + g) * (int64_t)GI_BLOCK_BYTES;
+}
+
+// byte offset of word w of SNP j in tile t, bounds-checked in debug builds
+__device__ inline int64_t word_offset_chk(const MatrixDesc& m, int64_t t, int64_t j, int w) {
+  GI_ASSERT(t >= 0 && t < m.T && j >= 0 && j < m.G * 32 && w >= 0 && w < 32);
+  const int L = (int)(j & 31);
+  return ((t * m.G + (j >> 5)) * (int64_t)GI_BLOCK_BYTES) + (int64_t)(((L ^ w) << 7) + (L << 2));
 }
 
 // byte offset of word w of SNP j in tile t

@@ -32,7 +32,7 @@ __global__ void upload_tiles_kernel(MatrixDesc m, uint8_t* __restrict__ x,
     }
     const int64_t t = wg >> 5;
     const int w = (int)(wg & 31);
-    *reinterpret_cast<uint32_t*>(x + word_offset(t, j, w, m.G)) = word;
+    *reinterpret_cast<uint32_t*>(x + word_offset_chk(m, t, j, w)) = word;
   }
 }
 
@@ -121,7 +121,7 @@ __global__ void synth_kernel(MatrixDesc m, uint8_t* __restrict__ x, uint64_t see
       if (um < tm) code = 1u;
       word |= code << (2 * s);
     }
-    *reinterpret_cast<uint32_t*>(x + word_offset(wg >> 5, j, (int)(wg & 31), m.G)) = word;
+    *reinterpret_cast<uint32_t*>(x + word_offset_chk(m, wg >> 5, j, (int)(wg & 31))) = word;
   }
 }
 
@@ -149,7 +149,8 @@ __global__ void stats_kernel(MatrixDesc m, const uint32_t* __restrict__ rowmask,
   const int64_t j = g * 32 + lane;
   int cnt = 0, s1 = 0, s2 = 0, miss = 0;
   for (int64_t t = 0; t < m.T; ++t) {
-    const uint8_t* blk = m.x + block_offset(t, g, m.G);
+    GI_ASSERT(g < m.G);
+  const uint8_t* blk = m.x + block_offset(t, g, m.G);
 #pragma unroll 8
     for (int q = 0; q < 32; ++q) {
       const uint32_t word = *reinterpret_cast<const uint32_t*>(blk + (q << 7) + (lane << 2));
@@ -237,11 +238,12 @@ __global__ void subset_rows_kernel(MatrixDesc src, MatrixDesc dst, uint8_t* __re
       const int64_t i = wg * 16 + s;
       if (i >= dst.n) break;
       const int64_t si = rows[i];
+      GI_ASSERT(si >= 0 && si < src.n);
       const uint32_t sw = *reinterpret_cast<const uint32_t*>(
-          src.x + word_offset(si >> 9, j, (int)((si >> 4) & 31), src.G));
+          src.x + word_offset_chk(src, si >> 9, j, (int)((si >> 4) & 31)));
       word |= ((sw >> (2 * (si & 15))) & 3u) << (2 * s);
     }
-    *reinterpret_cast<uint32_t*>(x + word_offset(wg >> 5, j, (int)(wg & 31), dst.G)) = word;
+    *reinterpret_cast<uint32_t*>(x + word_offset_chk(dst, wg >> 5, j, (int)(wg & 31))) = word;
   }
 }
 

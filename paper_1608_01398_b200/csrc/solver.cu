@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(
     get(i, key, sec);
     if (ge_thr(key, sec, tk, ts)) {
       const unsigned pos = atomicAdd(&s_pos, 1u);
+      GI_ASSERT(pos < kk);
       ok[pos] = key;
       oi[pos] = idx_base + lo + i;
       ov[pos] = topk_value(mode, beta, g, mu, lo + i);
