@@ -10,8 +10,8 @@ iterations per second.  The 25 GB matrix is far larger than the 126 MB L2, so
 every X^T r streams from HBM (no flush needed).
 
   value   device-resident: matrix, response and covariates already in HBM;
-          the native loop (gi_fit) runs each fit; CUDA events around the
-          timed fits, host syncs included (the loop is host-driven).
+          the native loop (gi_fit, or gi_fit_sharded under torchrun) runs each
+          fit; CUDA events around the timed fits, host syncs included.
   e2e     public API: fit(view, y, IhtConfig(k=20)) with y in pinned host
           memory; the response upload and the FitResult download are inside
           the timed region.
@@ -368,24 +368,14 @@ def main():
     from paper_1608_01398_b200 import iht as giht
 
     counters = {}
-    eng = None
-    if world == 1:
-        def run_fit():
-            return gi.fit(view, y, cfg, _resident=True)
-        gi.fit(view, y, cfg)  # primes the native loop's resident inputs
-    else:
-        state = gi.initial_state(view, y, cfg)
-        eng = state.engine
 
-        def run_fit():
-            return gi.fit(view, y, cfg, engine=eng)
+    def run_fit():
+        return gi.fit(view, y, cfg, _resident=True)
+    gi.fit(view, y, cfg)  # primes the native loop's resident inputs (sharded or not)
     with ClockSampler(local) as clocks:
         for _ in range(a.warmup):
             run_fit()
         torch.cuda.synchronize()
-        if eng is not None:
-            eng.aty_events = []
-            launches0 = eng.kernel_launches
         giht.profile_native(counters)
         iters = 0
         last = None
@@ -402,13 +392,8 @@ def main():
         barrier()
         giht.profile_native(None)
     ms = e0.elapsed_time(e1)
-    if eng is not None:
-        aty_ms = [st.elapsed_time(en) for st, en in eng.aty_events]
-        launches = eng.kernel_launches - launches0
-        eng.aty_events = None
-    else:
-        aty_ms = [counters["aty_ms"] / max(counters["aty_launches"], 1)]
-        launches = counters["kernel_launches"]
+    aty_ms = [counters["aty_ms"] / max(counters["aty_launches"], 1)]
+    launches = counters["kernel_launches"]
     if world > 1:
         ms = comm.allreduce_max(ms)
     value = iters / (ms / 1e3)

@@ -208,6 +208,31 @@ int gi_fit(gi_matrix *h, const double *y, const double *C, int64_t c, const uint
            const double *u, const double *v, const gi_fit_config *cfg, const int64_t *warm_idx,
            const double *warm_w, int64_t warm_k, const double *bcov0, gi_fit_result *res);
 
+/* ------------------------------------------------ SNP-sharded native loop */
+/* One process per GPU, each holding a contiguous SNP block [j_base, j_base +
+ * p_local) of the matrix.  The shards exchange only the
+ * n-length partial products X_S w (all-reduce, in place on the device), max|g|
+ * with the support's gradient entries, and the k top-k candidates per shard
+ * (all-gathers); every rank takes identical decisions. */
+typedef struct gi_comm gi_comm;
+/* host collectives supplied by the caller (e.g. torch.distributed / gloo):
+ * in-place all-reduce (op 0 sum, 1 max) and rank-major all-gather */
+typedef int (*gi_comm_allreduce_fn)(void *ctx, double *buf, int64_t count, int op);
+typedef int (*gi_comm_allgather_fn)(void *ctx, const double *send, int64_t count, double *recv);
+int gi_comm_nccl_available(void);
+/* 128-byte ncclUniqueId from rank 0, to be broadcast to the other ranks */
+int gi_comm_nccl_unique_id(uint8_t *out);
+int gi_comm_create_nccl(const uint8_t *id, int world, int rank, int device, gi_comm **out);
+int gi_comm_create_callbacks(int world, int rank, void *ctx, gi_comm_allreduce_fn allreduce,
+                             gi_comm_allgather_fn allgather, gi_comm **out);
+int gi_comm_free(gi_comm *comm);
+/* gi_fit over the local shard h (global SNP indices in warm_idx and in the
+ * result), joined through comm; y, C, keep, bcov0 are replicated. */
+int gi_fit_sharded(gi_matrix *h, gi_comm *comm, int64_t j_base, const double *y, const double *C,
+                   int64_t c, const uint8_t *keep, const double *u, const double *v,
+                   const gi_fit_config *cfg, const int64_t *warm_idx, const double *warm_w,
+                   int64_t warm_k, const double *bcov0, gi_fit_result *res);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,10 @@ class FitConfig(ctypes.Structure):
                 ("max_backtracks", c_i64), ("flags", c_i64)]
 
 
+ALLREDUCE_FN = ctypes.CFUNCTYPE(c_int, c_vp, ctypes.POINTER(c_dbl), c_i64, c_int)
+ALLGATHER_FN = ctypes.CFUNCTYPE(c_int, c_vp, ctypes.POINTER(c_dbl), c_i64, ctypes.POINTER(c_dbl))
+
+
 class FitOut(ctypes.Structure):
     """gi_fit_result (FitResult, iht.py:172-180)."""
 
@@ -89,6 +93,13 @@ def _declare(lib):
         "gi_dev_gather": ([c_i64, P, P, P, P], c_int),
         "gi_fit": ([P, P, P, c_i64, P, P, P, ctypes.POINTER(FitConfig), P, P, c_i64, P,
                     ctypes.POINTER(FitOut)], c_int),
+        "gi_fit_sharded": ([P, P, c_i64, P, P, c_i64, P, P, P, ctypes.POINTER(FitConfig), P, P,
+                            c_i64, P, ctypes.POINTER(FitOut)], c_int),
+        "gi_comm_nccl_available": ([], c_int),
+        "gi_comm_nccl_unique_id": ([P], c_int),
+        "gi_comm_create_nccl": ([P, c_int, c_int, c_int, P], c_int),
+        "gi_comm_create_callbacks": ([c_int, c_int, P, P, P, P], c_int),
+        "gi_comm_free": ([P], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

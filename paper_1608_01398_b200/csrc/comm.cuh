@@ -1,0 +1,25 @@
+// Internal definition of gi_comm (see comm.cu).  Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/genoiht_cuda.h"
+
+struct gi_comm {
+  enum Kind { kNccl = 0, kCallbacks = 1 };
+  int kind = kCallbacks;
+  int world = 1, rank = 0, device = 0;
+  void* nccl_comm = nullptr;  // ncclComm_t
+  void* ctx = nullptr;
+  gi_comm_allreduce_fn allreduce = nullptr;
+  gi_comm_allgather_fn allgather = nullptr;
+  double* scratch = nullptr;
+  int64_t scratch_doubles = 0;
+
+  // in-place all-reduce of a device buffer on stream s (op 0 = sum, 1 = max)
+  int allreduce_device(double* dbuf, int64_t count, int op, cudaStream_t s);
+  // all-gather of host buffers: recv = world x count, rank-major
+  int allgather_host(const double* send, int64_t count, double* recv, cudaStream_t s);
+  ~gi_comm();
+};

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/genoiht_cuda.h"
+#include "comm.cuh"
 #include "handle.cuh"
 
 namespace {
@@ -107,7 +108,7 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   TRY(ws->dalloc(ws->dw, 4 * (4 * kcap + 16)));
   GI_CUDA_TRY(cudaMemsetAsync(ws->ticket, 0, sizeof(uint32_t), ws->stream));
   GI_CUDA_TRY(cudaMallocHost(&ws->hin, sizeof(double) * (size_t)(8 * (4 * kcap + 16) + 4 * 64)));
-  GI_CUDA_TRY(cudaMallocHost(&ws->hout, sizeof(double) * (size_t)(8 + 2 * c + 4 * kcap + 64)));
+  GI_CUDA_TRY(cudaMallocHost(&ws->hout, sizeof(double) * (size_t)(8 + 2 * c + 6 * kcap + 64)));
   out = ws;
   return 0;
 }
@@ -119,8 +120,25 @@ struct Pair {
 
 class NativeFit {
  public:
-  NativeFit(gi_matrix* h, FitWs* ws, const gi_fit_config* cfg, bool masked, double n_eff)
-      : h_(h), ws_(ws), cfg_(*cfg), masked_(masked), n_eff_(n_eff) {}
+  NativeFit(gi_matrix* h, FitWs* ws, const gi_fit_config* cfg, bool masked, double n_eff,
+            gi_comm* comm, int64_t j_base)
+      : h_(h), ws_(ws), cfg_(*cfg), masked_(masked), n_eff_(n_eff), comm_(comm),
+        j_base_(j_base) {}
+
+  bool sharded() const { return comm_ != nullptr && comm_->world > 1; }
+
+  // entries of a global sparse vector owned by this shard, as local indices
+  void local_part(const std::vector<int64_t>& idx, const std::vector<double>& w,
+                  std::vector<int64_t>& li, std::vector<double>& lw) const {
+    li.clear();
+    lw.clear();
+    const int64_t lo = j_base_, hi = j_base_ + ws_->p;
+    for (size_t t = 0; t < idx.size(); ++t)
+      if (idx[t] >= lo && idx[t] < hi) {
+        li.push_back(idx[t] - lo);
+        lw.push_back(w[t]);
+      }
+  }
 
   int launches = 0;
   int aty_launches = 0;
@@ -170,11 +188,17 @@ class NativeFit {
     const gi::MatrixDesc d = h_->desc();
     cudaStream_t s = ws_->stream;
     const bool has_fit = !sup.empty();
+    std::vector<int64_t> lsup;
+    std::vector<double> lw;
+    local_part(sup, w, lsup, lw);
     if (has_fit) {
-      // the upload buffers are reused below for the gather, so sync the ax inputs first
-      TRY(upload_sparse(sup, w, 0));
-      TRY(gi::launch_ax(d, ws_->u, ws_->v, didx(0), dw(0), (int64_t)sup.size(), ws_->fitb, 0, s));
+      // slot 0 keeps the (local) support for the gather below
+      TRY(upload_sparse(lsup, lw, 0));
+      TRY(gi::launch_ax(d, ws_->u, ws_->v, didx(0), dw(0), (int64_t)lsup.size(), ws_->fitb, 0,
+                        s));
       ++launches;
+      // X_S b summed over the shards (NCCL in place on this stream)
+      if (sharded()) TRY(comm_->allreduce_device(ws_->fitb, ws_->n, 0, s));
     }
     TRY(upload_cov(bcov));
     const uint8_t* keep = masked_ ? ws_->keep : nullptr;
@@ -198,9 +222,9 @@ class NativeFit {
                              ws_->partials, ws_->ticket, s));
       ++launches;
     }
-    const int64_t ks = (int64_t)sup.size();
+    const int64_t ks = (int64_t)lsup.size();
     if (ks) {
-      // slot 0 still holds the support (uploaded above, stream-ordered)
+      // slot 0 still holds the local support (uploaded above, stream-ordered)
       TRY(gi::launch_gather(ks, didx(0), ws_->g, ws_->oval, s));
       ++launches;
     }
@@ -221,7 +245,25 @@ class NativeFit {
     loss = ho[0];
     gmax = ws_->p ? ho[3] : 0.0;
     gcov.assign(ho + 8, ho + 8 + ws_->c);
-    gsup.assign(ho + 8 + ws_->c, ho + 8 + ws_->c + ks);
+    if (!sharded()) {
+      gsup.assign(ho + 8 + ws_->c, ho + 8 + ws_->c + ks);
+      return 0;
+    }
+    // one all-gather carries max|g| and the support's gradient entries; each
+    // entry lives on exactly one shard, so summing the zero-padded rows is exact
+    const int64_t kg = (int64_t)sup.size();
+    std::vector<double> mine((size_t)(1 + kg), 0.0), all((size_t)((1 + kg) * comm_->world));
+    mine[0] = gmax;
+    for (int64_t t = 0, l = 0; t < kg; ++t)
+      if (sup[t] >= j_base_ && sup[t] < j_base_ + ws_->p) mine[1 + t] = ho[8 + ws_->c + l++];
+    TRY(comm_->allgather_host(mine.data(), 1 + kg, all.data(), s));
+    gmax = 0.0;
+    gsup.assign((size_t)kg, 0.0);
+    for (int r = 0; r < comm_->world; ++r) {
+      const double* row = all.data() + (size_t)r * (1 + kg);
+      gmax = std::max(gmax, row[0]);
+      for (int64_t t = 0; t < kg; ++t) gsup[t] += row[1 + t];
+    }
     return 0;
   }
 
@@ -230,9 +272,13 @@ class NativeFit {
                     const std::vector<double>* wcov) {
     const gi::MatrixDesc d = h_->desc();
     cudaStream_t s = ws_->stream;
-    TRY(upload_sparse(idx, w, 1));
-    TRY(gi::launch_ax(d, ws_->u, ws_->v, didx(1), dw(1), (int64_t)idx.size(), ws_->img, 0, s));
+    std::vector<int64_t> li;
+    std::vector<double> lw;
+    local_part(idx, w, li, lw);
+    TRY(upload_sparse(li, lw, 1));
+    TRY(gi::launch_ax(d, ws_->u, ws_->v, didx(1), dw(1), (int64_t)li.size(), ws_->img, 0, s));
     ++launches;
+    if (sharded()) TRY(comm_->allreduce_device(ws_->img, ws_->n, 0, s));
     if (wcov && ws_->c) {
       TRY(upload_cov(*wcov));
       TRY(gi::launch_add_cov(ws_->n, ws_->C, (int)ws_->c, ws_->cvec, ws_->img, s));
@@ -263,6 +309,8 @@ class NativeFit {
   int topk(int mode, double mu, int64_t k, std::vector<Pair>& out, double* den_mu = nullptr) {
     out.clear();
     cudaStream_t s = ws_->stream;
+    const int64_t ke = std::min(k, ws_->kcap);
+    std::vector<uint64_t> keys;
     if (ws_->p == 0 || k <= 0) {
       if (den_mu) {
         GI_CUDA_TRY(cudaMemcpyAsync(ws_->hout, ws_->scal + 4, 2 * sizeof(double),
@@ -271,36 +319,79 @@ class NativeFit {
         den_mu[0] = ws_->hout[0];
         den_mu[1] = ws_->hout[1];
       }
-      return 0;
-    }
-    const int64_t ke = std::min(k, ws_->kcap);
-    TRY(gi::launch_topk(ws_->p, ke, mode, ws_->beta, ws_->g, mu, 0, ws_->ckey, ws_->cidx,
-                        ws_->cval, ws_->oidx, ws_->oval, nullptr, ws_->ocnt, s,
-                        den_mu ? ws_->scal + 5 : nullptr));
-    launches += 2;
-    double* ho = ws_->hout;
-    if (den_mu)
-      GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + 2 * ke, ws_->scal + 4, 2 * sizeof(double),
+    } else {
+      TRY(gi::launch_topk(ws_->p, ke, mode, ws_->beta, ws_->g, mu, j_base_, ws_->ckey, ws_->cidx,
+                          ws_->cval, ws_->oidx, ws_->oval, ws_->okey, ws_->ocnt, s,
+                          den_mu ? ws_->scal + 5 : nullptr));
+      launches += 2;
+      double* ho = ws_->hout;
+      if (den_mu)
+        GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + 3 * ke, ws_->scal + 4, 2 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, s));
+      GI_CUDA_TRY(cudaMemcpyAsync(ho, ws_->ocnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      GI_CUDA_TRY(cudaMemcpyAsync(ho + 1, ws_->oidx, sizeof(int64_t) * ke, cudaMemcpyDeviceToHost,
+                                  s));
+      GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + ke, ws_->oval, sizeof(double) * ke,
                                   cudaMemcpyDeviceToHost, s));
-    GI_CUDA_TRY(cudaMemcpyAsync(ho, ws_->ocnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    GI_CUDA_TRY(cudaMemcpyAsync(ho + 1, ws_->oidx, sizeof(int64_t) * ke, cudaMemcpyDeviceToHost, s));
-    GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + ke, ws_->oval, sizeof(double) * ke,
-                                cudaMemcpyDeviceToHost, s));
-    TRY(sync());
-    int64_t cnt = 0;
-    memcpy(&cnt, ho, sizeof(int64_t));
-    const int64_t* hi = reinterpret_cast<const int64_t*>(ho + 1);
-    out.resize((size_t)cnt);
-    for (int64_t t = 0; t < cnt; ++t) out[t] = Pair{hi[t], ho[1 + ke + t]};
-    if (den_mu) {
-      den_mu[0] = ho[1 + 2 * ke];
-      den_mu[1] = ho[2 + 2 * ke];
+      if (sharded())
+        GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + 2 * ke, ws_->okey, sizeof(uint64_t) * ke,
+                                    cudaMemcpyDeviceToHost, s));
+      TRY(sync());
+      int64_t cnt = 0;
+      memcpy(&cnt, ho, sizeof(int64_t));
+      const int64_t* hi = reinterpret_cast<const int64_t*>(ho + 1);
+      const uint64_t* hk = reinterpret_cast<const uint64_t*>(ho + 1 + 2 * ke);
+      out.resize((size_t)cnt);
+      for (int64_t t = 0; t < cnt; ++t) out[t] = Pair{hi[t], ho[1 + ke + t]};
+      if (sharded()) keys.assign(hk, hk + cnt);
+      if (den_mu) {
+        den_mu[0] = ho[1 + 3 * ke];
+        den_mu[1] = ho[2 + 3 * ke];
+      }
     }
+    if (sharded() && ke > 0) TRY(merge_shards(out, keys, ke));
     std::sort(out.begin(), out.end(), [](const Pair& a, const Pair& b) { return a.idx < b.idx; });
     return 0;
   }
 
-  int scatter_beta(const std::vector<int64_t>& idx, const std::vector<double>& w) {
+  // Global top-k from the shards' local top-k lists: every shard's list is its
+  // exact top-k under (|value| desc, index asc), so the union holds the global
+  // one.  One all-gather of (key bits, index, value) triples, merged identically
+  // on every rank.
+  int merge_shards(std::vector<Pair>& out, const std::vector<uint64_t>& keys, int64_t ke) {
+    std::vector<double> mine((size_t)(3 * ke), 0.0), all((size_t)(3 * ke * comm_->world));
+    for (size_t t = 0; t < out.size(); ++t) {
+      memcpy(&mine[3 * t], &keys[t], 8);
+      memcpy(&mine[3 * t + 1], &out[t].idx, 8);
+      mine[3 * t + 2] = out[t].val;
+    }
+    TRY(comm_->allgather_host(mine.data(), 3 * ke, all.data(), ws_->stream));
+    struct Cand {
+      uint64_t key;
+      int64_t idx;
+      double val;
+    };
+    std::vector<Cand> cands;
+    for (size_t e = 0; e < all.size(); e += 3) {
+      Cand c;
+      memcpy(&c.key, &all[e], 8);
+      memcpy(&c.idx, &all[e + 1], 8);
+      c.val = all[e + 2];
+      if (c.key != 0) cands.push_back(c);  // 0 marks an empty slot
+    }
+    std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+      return a.key != b.key ? a.key > b.key : a.idx < b.idx;
+    });
+    if ((int64_t)cands.size() > ke) cands.resize((size_t)ke);
+    out.clear();
+    for (const Cand& c : cands) out.push_back(Pair{c.idx, c.val});
+    return 0;
+  }
+
+  int scatter_beta(const std::vector<int64_t>& idx_g, const std::vector<double>& w_g) {
+    std::vector<int64_t> idx;
+    std::vector<double> w;
+    local_part(idx_g, w_g, idx, w);
     if (idx.empty()) return 0;
     TRY(upload_sparse(idx, w, 2));
     TRY(gi::launch_scatter((int64_t)idx.size(), didx(2), dw(2), ws_->beta, ws_->stream));
@@ -314,6 +405,8 @@ class NativeFit {
   gi_fit_config cfg_;
   bool masked_;
   double n_eff_;
+  gi_comm* comm_;
+  int64_t j_base_;
 };
 
 double dot(const std::vector<double>& a) {
@@ -330,10 +423,11 @@ bool any_nonzero(const std::vector<double>& a) {
 
 }  // namespace
 
-extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
-                      const uint8_t* keep, const double* u, const double* v,
-                      const gi_fit_config* cfg, const int64_t* warm_idx, const double* warm_w,
-                      int64_t warm_k, const double* bcov0, gi_fit_result* res) {
+static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y,
+                    const double* C, int64_t c, const uint8_t* keep, const double* u,
+                    const double* v, const gi_fit_config* cfg, const int64_t* warm_idx,
+                    const double* warm_w, int64_t warm_k, const double* bcov0,
+                    gi_fit_result* res) {
   CHECK_ARG(h && cfg && res, "NULL argument");
   CHECK_ARG(c >= 0 && c <= 64, "the native loop supports at most 64 covariate columns");
   CHECK_ARG(c == 0 || C != nullptr, "covariate matrix is NULL");
@@ -418,7 +512,7 @@ extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
   ws->n_eff = n_eff;
   }
 
-  NativeFit F(h, ws.get(), cfg, masked, n_eff);
+  NativeFit F(h, ws.get(), cfg, masked, n_eff, comm, j_base);
   struct EventPair {
     cudaEvent_t a = nullptr, b = nullptr;
     ~EventPair() {
@@ -615,4 +709,22 @@ extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
   res->aty_ms_total = F.aty_ms;
   res->aty_launches = F.aty_launches;
   return 0;
+}
+
+extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
+                      const uint8_t* keep, const double* u, const double* v,
+                      const gi_fit_config* cfg, const int64_t* warm_idx, const double* warm_w,
+                      int64_t warm_k, const double* bcov0, gi_fit_result* res) {
+  return fit_impl(h, nullptr, 0, y, C, c, keep, u, v, cfg, warm_idx, warm_w, warm_k, bcov0, res);
+}
+
+extern "C" int gi_fit_sharded(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y,
+                              const double* C, int64_t c, const uint8_t* keep, const double* u,
+                              const double* v, const gi_fit_config* cfg,
+                              const int64_t* warm_idx, const double* warm_w, int64_t warm_k,
+                              const double* bcov0, gi_fit_result* res) {
+  CHECK_ARG(comm != nullptr, "NULL communicator");
+  CHECK_ARG(j_base >= 0, "negative SNP offset");
+  return fit_impl(h, comm, j_base, y, C, c, keep, u, v, cfg, warm_idx, warm_w, warm_k, bcov0,
+                  res);
 }

@@ -42,6 +42,9 @@ class LocalComm:
     def allgather_host(self, array: np.ndarray) -> list:
         return [np.asarray(array)]
 
+    def allreduce_host(self, array: np.ndarray, op: str) -> np.ndarray:
+        return np.asarray(array, dtype=np.float64)
+
 
 class TorchComm:
     """Collectives on the default process group.  Device buffers go straight to
@@ -94,6 +97,77 @@ class TorchComm:
         self.dist.all_gather(out, t, group=self.group)
         return [o.cpu().numpy() for o in out]
 
+    def allreduce_host(self, array: np.ndarray, op: str) -> np.ndarray:
+        import torch
+
+        t = torch.as_tensor(np.asarray(array, dtype=np.float64)).to(self._device())
+        red = self.dist.ReduceOp.SUM if op == "sum" else self.dist.ReduceOp.MAX
+        self.dist.all_reduce(t, op=red, group=self.group)
+        return t.cpu().numpy()
+
+
+class NativeComm:
+    """A gi_comm* for the native sharded loop (gi_fit_sharded).
+
+    With the NCCL backend the library runs its own NCCL communicator (rank 0's
+    unique id is broadcast over the torch process group) and reduces device
+    buffers in place on the fit's stream.  Otherwise (gloo: several ranks may
+    share one GPU) the library calls back into ``comm``'s host collectives."""
+
+    def __init__(self, comm, device: int):
+        import ctypes
+
+        from . import _native
+
+        self.comm = comm
+        self.raw = ctypes.c_void_p(0)
+        L = _native.lib()
+        use_nccl = getattr(comm, "backend", None) == "nccl" and L.gi_comm_nccl_available()
+        if use_nccl:
+            uid = (ctypes.c_uint8 * 128)()
+            if comm.rank == 0:
+                _native.check(L.gi_comm_nccl_unique_id(uid))
+            box = [bytes(uid)]
+            comm.dist.broadcast_object_list(box, src=0, group=comm.group)
+            uid = (ctypes.c_uint8 * 128).from_buffer_copy(box[0])
+            _native.check(L.gi_comm_create_nccl(uid, comm.world, comm.rank, device,
+                                                ctypes.byref(self.raw)))
+            self.kind = "nccl"
+        else:
+            def allreduce(_ctx, buf, count, op):
+                try:
+                    arr = np.ctypeslib.as_array(buf, shape=(count,))
+                    arr[:] = comm.allreduce_host(arr.copy(), "sum" if op == 0 else "max")
+                    return 0
+                except Exception:  # reported by the library as a failed collective
+                    return -1
+
+            def allgather(_ctx, send, count, recv):
+                try:
+                    src = np.ctypeslib.as_array(send, shape=(count,)).copy()
+                    dst = np.ctypeslib.as_array(recv, shape=(count * comm.world,))
+                    dst[:] = np.concatenate(comm.allgather_host(src))
+                    return 0
+                except Exception:
+                    return -1
+
+            # keep the ctypes thunks alive as long as the communicator
+            self._ar = _native.ALLREDUCE_FN(allreduce)
+            self._ag = _native.ALLGATHER_FN(allgather)
+            _native.check(L.gi_comm_create_callbacks(comm.world, comm.rank, None, self._ar,
+                                                     self._ag, ctypes.byref(self.raw)))
+            self.kind = "callbacks"
+
+    def __del__(self):
+        try:
+            from . import _native
+
+            if self.raw:
+                _native.lib().gi_comm_free(self.raw)
+                self.raw = None
+        except Exception:
+            pass
+
 
 def merge_topk(keys: np.ndarray, idx: np.ndarray, vals: np.ndarray, k: int):
     """Global top-k from per-shard candidate lists under (|value| desc, index asc).
@@ -142,6 +216,14 @@ class ShardedGenotypes:
         from .engine import Genotypes
 
         return Genotypes(self.local, j_base=self.j_base, p_global=self.p, comm=self.comm)
+
+    def native_comm(self) -> "NativeComm":
+        """The library-side communicator (created once per process group)."""
+        cached = getattr(self.comm, "_native_comm", None)
+        if cached is None:
+            cached = NativeComm(self.comm, self.device)
+            self.comm._native_comm = cached
+        return cached
 
     def ax_columns(self, idx, w) -> np.ndarray:
         idx = np.asarray(idx, dtype=np.int64)

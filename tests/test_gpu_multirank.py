@@ -1,5 +1,7 @@
 """The sharded DEVICE path on one GPU: two processes, each owning a contiguous
-SNP block (its own device-resident shard and DeviceEngine), joined by gloo.
+SNP block (its own device-resident shard), joined by gloo -- through the native
+sharded loop (gi_fit_sharded with host-callback collectives) and through the
+Python loop over DeviceEngine.
 Collectives are host-staged, so no kernel waits on another process.  The
 sharded fit must reproduce the unsharded device fit and the oracle: identical
 support and iteration count, weights and loss to 1e-6."""
@@ -23,7 +25,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, native):
     import torch
     import torch.distributed as dist
 
@@ -39,19 +41,22 @@ def _worker(rank, world, port, q):
         geno = ShardedGenotypes.synthetic(N, P, SEED, comm, device=0, missing_rate=0.01)
         view = gi.StandardizedView(geno, gi.CovariateBlock.build(None, n=N))
         y, truth = simulate_phenotype(view, SimulationSpec(k_true=K, seed=5))
-        res = gi.fit(view, y, gi.IhtConfig(k=K))
+        res = gi.fit(view, y, gi.IhtConfig(k=K), native=native)
+        if native:
+            assert geno.native_comm().kind == "callbacks"  # gloo: host-staged collectives
         q.put((rank, y, res.model.support, res.model.weights, res.model.covar, res.loss_trace,
                res.iterations, res.reason))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_shards_on_one_gpu_match_single_device_fit():
+@pytest.mark.parametrize("native", [True, False], ids=["native-sharded-loop", "python-loop"])
+def test_two_shards_on_one_gpu_match_single_device_fit(native):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, native)) for r in range(world)]
     for p_ in procs:
         p_.start()
     out = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
