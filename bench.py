@@ -341,7 +341,10 @@ def main():
     from paper_1608_01398_b200 import dist as gdist
     from paper_1608_01398_b200.simulate import SimulationSpec, simulate_phenotype
 
-    if world > 1:
+    # GI_FORCE_SHARDED=1 runs the sharded path (its communicator and exchange
+    # steps) also at world size 1, e.g. to exercise NCCL on a single GPU
+    sharded = world > 1 or os.environ.get("GI_FORCE_SHARDED") == "1"
+    if sharded:
         if backend == "nccl":
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -422,12 +425,12 @@ def main():
     e2e_value = e2e_iters / (e2e_ms / 1e3)
 
     if rank != 0:
-        if world > 1:
+        if sharded:
             torch.distributed.destroy_process_group()
         return
 
     # ---- roofline of the X^T r kernel
-    n, p_local = a.n, (geno.local.p if world > 1 else a.p)
+    n, p_local = a.n, (geno.local.p if sharded else a.p)
     nb = (n + 3) // 4
     alg_bytes = p_local * nb + 8 * n + 24 * p_local
     aty_avg = statistics.mean(aty_ms) if aty_ms else float("nan")
@@ -468,7 +471,7 @@ def main():
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         torch.distributed.destroy_process_group()
 
 

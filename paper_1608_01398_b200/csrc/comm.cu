@@ -67,12 +67,13 @@ NcclApi& nccl() {
 
 // ------------------------------------------------------------------ collectives
 int gi_comm::allreduce_device(double* dbuf, int64_t count, int op, cudaStream_t s) {
-  if (world <= 1 || count <= 0) return 0;
-  if (kind == kNccl) {
+  if (count <= 0) return 0;
+  if (kind == kNccl) {  // also at world 1: a real (local) NCCL collective
     NCCL_TRY(nccl().all_reduce(dbuf, dbuf, (size_t)count, ncclFloat64, op ? ncclMax : ncclSum,
                                static_cast<ncclComm_t>(nccl_comm), s));
     return 0;
   }
+  if (world <= 1) return 0;
   std::vector<double> host((size_t)count);
   GI_CUDA_TRY(cudaMemcpyAsync(host.data(), dbuf, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
   GI_CUDA_TRY(cudaStreamSynchronize(s));
@@ -86,11 +87,11 @@ int gi_comm::allreduce_device(double* dbuf, int64_t count, int op, cudaStream_t 
 }
 
 int gi_comm::allgather_host(const double* send, int64_t count, double* recv, cudaStream_t s) {
-  if (world <= 1) {
-    memcpy(recv, send, sizeof(double) * count);
-    return 0;
-  }
   if (kind == kCallbacks) {
+    if (world <= 1) {
+      memcpy(recv, send, sizeof(double) * count);
+      return 0;
+    }
     if (allgather(ctx, send, count, recv) != 0) {
       gi_set_error("host all-gather callback failed");
       return -1;

@@ -125,7 +125,9 @@ class NativeFit {
       : h_(h), ws_(ws), cfg_(*cfg), masked_(masked), n_eff_(n_eff), comm_(comm),
         j_base_(j_base) {}
 
-  bool sharded() const { return comm_ != nullptr && comm_->world > 1; }
+  // gi_fit_sharded always runs the exchange steps, also on a world of one
+  // (which is how the NCCL backend is exercised on a single GPU)
+  bool sharded() const { return comm_ != nullptr; }
 
   // entries of a global sparse vector owned by this shard, as local indices
   void local_part(const std::vector<int64_t>& idx, const std::vector<double>& w,

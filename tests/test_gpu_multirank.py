@@ -80,3 +80,59 @@ def test_two_shards_on_one_gpu_match_single_device_fit(native):
         np.testing.assert_allclose(weights, want.model.weights, rtol=1e-6)
         np.testing.assert_allclose(covar, want.model.covar, rtol=1e-6, atol=1e-12)
         np.testing.assert_allclose(trace, want.loss_trace, rtol=1e-6)
+
+
+def _nccl_worker(port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        import paper_1608_01398_b200 as gi
+        from paper_1608_01398_b200.dist import ShardedGenotypes, TorchComm
+        from paper_1608_01398_b200.simulate import SimulationSpec, simulate_phenotype
+
+        comm = TorchComm()
+        geno = ShardedGenotypes.synthetic(N, P, SEED, comm, device=0, missing_rate=0.01)
+        view = gi.StandardizedView(geno, gi.CovariateBlock.build(None, n=N))
+        y, _ = simulate_phenotype(view, SimulationSpec(k_true=K, seed=5))
+        out = {}
+        for native in (True, False):
+            res = gi.fit(view, y, gi.IhtConfig(k=K), native=native)
+            out[native] = (res.model.support, res.model.weights, res.model.covar,
+                           res.loss_trace, res.iterations, res.reason)
+        q.put((y, out, geno.native_comm().kind))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_backend_world_one_matches_device_fit():
+    """The NCCL communicator of the native sharded loop (dlopen'd libnccl,
+    in-place device all-reduce, device-staged all-gather) on a world of one:
+    gi_fit_sharded runs every exchange step through real NCCL collectives and
+    must reproduce the unsharded gi_fit bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    proc = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    proc.start()
+    y, out, kind = q.get(timeout=600)
+    proc.join(timeout=120)
+    assert proc.exitcode == 0
+    assert kind == "nccl"
+    import paper_1608_01398_b200 as gi
+
+    full = gi.PackedGenotypeMatrix.synthetic(N, P, SEED, missing_rate=0.01)
+    view = gi.StandardizedView(full, gi.CovariateBlock.build(None, n=N))
+    want = gi.fit(view, y, gi.IhtConfig(k=K))
+    for native, (support, weights, covar, trace, iters, reason) in out.items():
+        np.testing.assert_array_equal(support, want.model.support)
+        assert iters == want.iterations and reason == want.reason
+        if native:  # same kernels, same order: identical bits
+            np.testing.assert_array_equal(weights, want.model.weights)
+            np.testing.assert_array_equal(trace, want.loss_trace)
+        np.testing.assert_allclose(weights, want.model.weights, rtol=1e-6)
+        np.testing.assert_allclose(covar, want.model.covar, rtol=1e-6, atol=1e-12)
+        np.testing.assert_allclose(trace, want.loss_trace, rtol=1e-6)
