@@ -88,6 +88,26 @@ int launch_sumsq(int64_t m, const double* x, double* scal, int slot, double* par
                  unsigned int* ticket, cudaStream_t s);
 int launch_add_cov(int64_t n, const double* C, int c, const double* w, double* x,
                    cudaStream_t s);
+int launch_image_sumsq(int64_t m, const double* x, const double* C, int c, const double* w,
+                       const uint8_t* keep, double* scal, int slot, int ratio_out,
+                       double ratio_num, double* host_out, double* partials,
+                       unsigned int* ticket, cudaStream_t s);
+// segments of 8-byte words copied (or gathered through idx) to out[dst ...]
+constexpr int kMaxPub = 6;
+struct PubSeg {
+  const void* src;
+  const int64_t* idx;  // NULL: plain copy
+  int64_t count;
+  int64_t dst;
+};
+struct PubArgs {
+  PubSeg seg[kMaxPub];
+  int nseg = 0;
+  void add(const void* src, int64_t count, int64_t dst, const int64_t* idx = nullptr) {
+    if (count > 0) seg[nseg++] = PubSeg{src, idx, count, dst};
+  }
+};
+int launch_publish(const PubArgs& a, void* out, cudaStream_t s);
 int64_t topk_blocks(int64_t p);
 int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double* g, double mu,
                 int64_t idx_base, uint64_t* cand_key, int64_t* cand_idx, double* cand_val,

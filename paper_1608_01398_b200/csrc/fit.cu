@@ -9,7 +9,11 @@
 // case through the same kernels).  Every O(n), O(p) and O(n p) operation is a
 // kernel on the matrix's device; the host keeps the O(k) support bookkeeping
 // and recomputes the candidate step with the reference's float operations.
-// One host sync per phase (refresh, image, top-k).
+// One host sync per phase (refresh, image, top-k).  Each phase's host inputs
+// (sparse vectors, covariate weights) are staged in a pinned arena and reach
+// the device in ONE copy; its results come back through mapped host memory,
+// written by the phase's last kernel -- no per-array copy-engine transfers,
+// which at small n cost more than the kernels themselves.
 #include <stdint.h>
 #include <string.h>
 
@@ -35,12 +39,17 @@ struct FitWs {
   uint8_t* keep = nullptr;
   int32_t* s1cnt = nullptr;
   uint32_t *ticket = nullptr, *rowmask = nullptr;
-  uint64_t *ckey = nullptr, *okey = nullptr;
-  int64_t *cidx = nullptr, *oidx = nullptr, *ocnt = nullptr, *didx = nullptr;
-  double *cval = nullptr, *oval = nullptr, *dw = nullptr;
-  // pinned host staging
-  double* hin = nullptr;   // uploads: idx | w | cov (kcap + kcap + 8)
-  double* hout = nullptr;  // downloads
+  uint64_t* ckey = nullptr;
+  int64_t* cidx = nullptr;
+  double* cval = nullptr;
+  // uploads: pinned host arena mirrored byte for byte by a device arena
+  char* hin = nullptr;
+  char* din = nullptr;
+  size_t in_cap = 0, in_off = 0, in_flushed = 0;
+  // results: mapped pinned host memory written by kernels (device alias dmap)
+  double* hmap = nullptr;
+  double* dmap = nullptr;
+  int64_t oR = 0, oT = 0, oM = 0, oS = 0;  // regions: refresh, top-k, den/mu, image
   std::vector<void*> dev_allocs;
   bool primed = false, masked = false;
   double n_eff = 0.0;
@@ -52,7 +61,7 @@ struct FitWs {
     for (void* ptr : dev_allocs) cudaFreeAsync(ptr, stream);
     if (stream) cudaStreamSynchronize(stream);
     if (hin) cudaFreeHost(hin);
-    if (hout) cudaFreeHost(hout);
+    if (hmap) cudaFreeHost(hmap);
     if (stream) cudaStreamDestroy(stream);
     cudaSetDevice(prev);
   }
@@ -100,15 +109,19 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   TRY(ws->dalloc(ws->ckey, ws->slots));
   TRY(ws->dalloc(ws->cidx, ws->slots));
   TRY(ws->dalloc(ws->cval, ws->slots));
-  TRY(ws->dalloc(ws->okey, kcap));
-  TRY(ws->dalloc(ws->oidx, kcap));
-  TRY(ws->dalloc(ws->oval, kcap));
-  TRY(ws->dalloc(ws->ocnt, 1));
-  TRY(ws->dalloc(ws->didx, 4 * (4 * kcap + 16)));
-  TRY(ws->dalloc(ws->dw, 4 * (4 * kcap + 16)));
+  // between two syncs a phase stages at most ~3 sparse vectors of <= 2 kcap
+  // entries plus one covariate vector; the arena is reset at every sync
+  ws->in_cap = (size_t)(128 * kcap + 64) * sizeof(double);
+  TRY(ws->dalloc(ws->din, (int64_t)ws->in_cap));
   GI_CUDA_TRY(cudaMemsetAsync(ws->ticket, 0, sizeof(uint32_t), ws->stream));
-  GI_CUDA_TRY(cudaMallocHost(&ws->hin, sizeof(double) * (size_t)(8 * (4 * kcap + 16) + 4 * 64)));
-  GI_CUDA_TRY(cudaMallocHost(&ws->hout, sizeof(double) * (size_t)(8 + 2 * c + 6 * kcap + 64)));
+  GI_CUDA_TRY(cudaMallocHost(&ws->hin, ws->in_cap));
+  ws->oR = 0;                          // scal[0..8) | g_cov (c) | g on the support (kcap)
+  ws->oT = 8 + c + kcap;               // count | idx (kcap) | val (kcap) | key (kcap)
+  ws->oM = ws->oT + 1 + 3 * kcap;      // den, mu
+  ws->oS = ws->oM + 2;                 // ||X d||^2 of a backtracking check
+  GI_CUDA_TRY(cudaHostAlloc(&ws->hmap, sizeof(double) * (size_t)(ws->oS + 2),
+                            cudaHostAllocMapped));
+  GI_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ws->dmap), ws->hmap, 0));
   out = ws;
   return 0;
 }
@@ -147,41 +160,40 @@ class NativeFit {
   double aty_ms = 0.0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
-  // Upload a sparse vector (idx, w) into the device slot `slot` (0..3).  Each
-  // slot has its own pinned staging region, so several uploads may be in
-  // flight between two syncs without the host overwriting unread bytes.
-  int upload_sparse(const std::vector<int64_t>& idx, const std::vector<double>& w, int slot = 0) {
-    const int64_t k = (int64_t)idx.size();
-    if (k == 0) return 0;
-    const int64_t cap = 4 * ws_->kcap + 16;  // per slot: idx | w
-    int64_t* hi = reinterpret_cast<int64_t*>(ws_->hin + slot * 2 * cap);
-    double* hw = ws_->hin + slot * 2 * cap + cap;
-    memcpy(hi, idx.data(), sizeof(int64_t) * k);
-    memcpy(hw, w.data(), sizeof(double) * k);
-    GI_CUDA_TRY(cudaMemcpyAsync(ws_->didx + slot * cap, hi, sizeof(int64_t) * k,
-                                cudaMemcpyHostToDevice, ws_->stream));
-    GI_CUDA_TRY(cudaMemcpyAsync(ws_->dw + slot * cap, hw, sizeof(double) * k,
-                                cudaMemcpyHostToDevice, ws_->stream));
+  // Stage `count` items for the device: copied into the pinned arena now, sent
+  // by the next flush(); the returned device pointer is valid until the next
+  // sync().
+  template <typename T>
+  int stage(const T* src, int64_t count, const T*& dev) {
+    const size_t bytes = sizeof(T) * (size_t)count;
+    const size_t off = (ws_->in_off + 15) & ~(size_t)15;
+    if (off + bytes > ws_->in_cap) {
+      gi_set_error("internal: staging arena overflow");
+      return -1;
+    }
+    if (bytes) memcpy(ws_->hin + off, src, bytes);
+    ws_->in_off = off + bytes;
+    dev = reinterpret_cast<const T*>(ws_->din + off);
     return 0;
   }
-  int64_t* didx(int slot) { return ws_->didx + slot * (4 * ws_->kcap + 16); }
-  double* dw(int slot) { return ws_->dw + slot * (4 * ws_->kcap + 16); }
-
-  int upload_cov(const std::vector<double>& cv) {
-    if (ws_->c == 0) return 0;
-    double* hc = ws_->hin + 4 * 2 * (4 * ws_->kcap + 16) + cov_slot_ * 64;
-    cov_slot_ = (cov_slot_ + 1) & 3;
-    memcpy(hc, cv.data(), sizeof(double) * ws_->c);
-    GI_CUDA_TRY(cudaMemcpyAsync(ws_->cvec, hc, sizeof(double) * ws_->c, cudaMemcpyHostToDevice,
-                                ws_->stream));
+  int flush() {
+    if (ws_->in_off > ws_->in_flushed) {
+      GI_CUDA_TRY(cudaMemcpyAsync(ws_->din + ws_->in_flushed, ws_->hin + ws_->in_flushed,
+                                  ws_->in_off - ws_->in_flushed, cudaMemcpyHostToDevice,
+                                  ws_->stream));
+      ws_->in_flushed = ws_->in_off;
+    }
     return 0;
   }
-
   int sync() {
     GI_CUDA_TRY(cudaStreamSynchronize(ws_->stream));
+    ws_->in_off = ws_->in_flushed = 0;  // every staged copy has landed
     return 0;
   }
-  int cov_slot_ = 0;
+  // beta entries to write before the next refresh (staged by scatter_beta)
+  const int64_t* pend_idx_ = nullptr;
+  const double* pend_w_ = nullptr;
+  int64_t pend_k_ = 0;
 
   // _refresh_state: returns loss, max|g|, g_cov, g on the support
   int refresh(const std::vector<int64_t>& sup, const std::vector<double>& w,
@@ -193,19 +205,27 @@ class NativeFit {
     std::vector<int64_t> lsup;
     std::vector<double> lw;
     local_part(sup, w, lsup, lw);
+    // one upload for the pending beta update, the support and b_cov
+    const int64_t* d_sup = nullptr;
+    const double *d_w = nullptr, *d_cov = nullptr;
+    TRY(stage(lsup.data(), (int64_t)lsup.size(), d_sup));
+    TRY(stage(lw.data(), (int64_t)lw.size(), d_w));
+    TRY(stage(bcov.data(), ws_->c, d_cov));
+    TRY(flush());
+    if (pend_k_) {
+      TRY(gi::launch_scatter(pend_k_, pend_idx_, pend_w_, ws_->beta, s));
+      ++launches;
+      pend_k_ = 0;
+    }
     if (has_fit) {
-      // slot 0 keeps the (local) support for the gather below
-      TRY(upload_sparse(lsup, lw, 0));
-      TRY(gi::launch_ax(d, ws_->u, ws_->v, didx(0), dw(0), (int64_t)lsup.size(), ws_->fitb, 0,
-                        s));
+      TRY(gi::launch_ax(d, ws_->u, ws_->v, d_sup, d_w, (int64_t)lsup.size(), ws_->fitb, 0, s));
       ++launches;
       // X_S b summed over the shards (NCCL in place on this stream)
       if (sharded()) TRY(comm_->allreduce_device(ws_->fitb, ws_->n, 0, s));
     }
-    TRY(upload_cov(bcov));
     const uint8_t* keep = masked_ ? ws_->keep : nullptr;
     TRY(gi::launch_residual(ws_->n, ws_->y, has_fit ? ws_->fitb : nullptr,
-                            ws_->c ? ws_->C : nullptr, (int)ws_->c, ws_->cvec, keep, n_eff_,
+                            ws_->c ? ws_->C : nullptr, (int)ws_->c, d_cov, keep, n_eff_,
                             ws_->r, ws_->scal, ws_->partials, ws_->ticket, s));
     TRY(gi::launch_center(ws_->n, ws_->npad, ws_->r, keep, ws_->scal, ws_->rt, ws_->partials,
                           ws_->ticket, s));
@@ -224,21 +244,16 @@ class NativeFit {
                              ws_->partials, ws_->ticket, s));
       ++launches;
     }
+    // scal, g_cov and g on the (local) support -> mapped host memory, one launch
     const int64_t ks = (int64_t)lsup.size();
-    if (ks) {
-      // slot 0 still holds the local support (uploaded above, stream-ordered)
-      TRY(gi::launch_gather(ks, didx(0), ws_->g, ws_->oval, s));
-      ++launches;
-    }
-    double* ho = ws_->hout;
-    GI_CUDA_TRY(cudaMemcpyAsync(ho, ws_->scal, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
-    if (ws_->c)
-      GI_CUDA_TRY(cudaMemcpyAsync(ho + 8, ws_->cvec + ws_->c, sizeof(double) * ws_->c,
-                                  cudaMemcpyDeviceToHost, s));
-    if (ks)
-      GI_CUDA_TRY(cudaMemcpyAsync(ho + 8 + ws_->c, ws_->oval, sizeof(double) * ks,
-                                  cudaMemcpyDeviceToHost, s));
+    gi::PubArgs pub;
+    pub.add(ws_->scal, 8, ws_->oR);
+    pub.add(ws_->cvec + ws_->c, ws_->c, ws_->oR + 8);
+    pub.add(ws_->g, ks, ws_->oR + 8 + ws_->c, d_sup);
+    TRY(gi::launch_publish(pub, ws_->dmap, s));
+    ++launches;
     TRY(sync());
+    const double* ho = ws_->hmap + ws_->oR;
     if (ev0 && ws_->p) {
       float ms = 0.f;
       GI_CUDA_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
@@ -269,87 +284,75 @@ class NativeFit {
     return 0;
   }
 
-  // || X_idx w + C wcov ||^2 over the view's rows -> scal[4] (enqueue only)
+  // || X_idx w + C wcov ||^2 over the view's rows -> scal[4] (enqueue only).
+  // ratio_out >= 0: also scal[ratio_out] = ratio_num / scal[4]; host_out
+  // (mapped) receives {scal[4], ratio}.
   int image_enqueue(const std::vector<int64_t>& idx, const std::vector<double>& w,
-                    const std::vector<double>* wcov) {
+                    const std::vector<double>* wcov, int ratio_out, double ratio_num,
+                    double* host_out) {
     const gi::MatrixDesc d = h_->desc();
     cudaStream_t s = ws_->stream;
     std::vector<int64_t> li;
     std::vector<double> lw;
     local_part(idx, w, li, lw);
-    TRY(upload_sparse(li, lw, 1));
-    TRY(gi::launch_ax(d, ws_->u, ws_->v, didx(1), dw(1), (int64_t)li.size(), ws_->img, 0, s));
+    const int64_t* d_idx = nullptr;
+    const double *d_w = nullptr, *d_cov = nullptr;
+    TRY(stage(li.data(), (int64_t)li.size(), d_idx));
+    TRY(stage(lw.data(), (int64_t)lw.size(), d_w));
+    const bool cov = wcov && ws_->c;
+    if (cov) TRY(stage(wcov->data(), ws_->c, d_cov));
+    TRY(flush());
+    TRY(gi::launch_ax(d, ws_->u, ws_->v, d_idx, d_w, (int64_t)li.size(), ws_->img, 0, s));
     ++launches;
     if (sharded()) TRY(comm_->allreduce_device(ws_->img, ws_->n, 0, s));
-    if (wcov && ws_->c) {
-      TRY(upload_cov(*wcov));
-      TRY(gi::launch_add_cov(ws_->n, ws_->C, (int)ws_->c, ws_->cvec, ws_->img, s));
-      ++launches;
-    }
-    if (masked_) {
-      TRY(gi::launch_mask(ws_->n, ws_->keep, ws_->img, s));
-      ++launches;
-    }
-    TRY(gi::launch_sumsq(ws_->n, ws_->img, ws_->scal, 4, ws_->partials, ws_->ticket, s));
+    // + C wcov, row mask and the squared norm in one pass
+    TRY(gi::launch_image_sumsq(ws_->n, ws_->img, cov ? ws_->C : nullptr, cov ? (int)ws_->c : 0,
+                               d_cov, masked_ ? ws_->keep : nullptr, ws_->scal, 4, ratio_out,
+                               ratio_num, host_out, ws_->partials, ws_->ticket, s));
     ++launches;
     return 0;
   }
 
   int image_sumsq(const std::vector<int64_t>& idx, const std::vector<double>& w,
                   const std::vector<double>* wcov, double& out) {
-    TRY(image_enqueue(idx, w, wcov));
-    GI_CUDA_TRY(cudaMemcpyAsync(ws_->hout, ws_->scal + 4, sizeof(double), cudaMemcpyDeviceToHost,
-                                ws_->stream));
+    TRY(image_enqueue(idx, w, wcov, -1, 0.0, ws_->dmap + ws_->oS));
     TRY(sync());
-    out = ws_->hout[0];
+    out = ws_->hmap[ws_->oS];
     return 0;
   }
 
   // k largest |g| (mode 0) or |beta - mu g| (mode 1), sorted by index
-  // `mu_dev` (optional): take mu from the device (scal[5]) and also return
-  // scal[4] (den) and scal[5] (mu) through `den_mu` in the same sync
+  // `den_mu` (optional): take mu from the device (scal[5], written by the
+  // preceding image_enqueue) and return den and mu from the same sync
   int topk(int mode, double mu, int64_t k, std::vector<Pair>& out, double* den_mu = nullptr) {
     out.clear();
     cudaStream_t s = ws_->stream;
     const int64_t ke = std::min(k, ws_->kcap);
     std::vector<uint64_t> keys;
     if (ws_->p == 0 || k <= 0) {
-      if (den_mu) {
-        GI_CUDA_TRY(cudaMemcpyAsync(ws_->hout, ws_->scal + 4, 2 * sizeof(double),
-                                    cudaMemcpyDeviceToHost, s));
-        TRY(sync());
-        den_mu[0] = ws_->hout[0];
-        den_mu[1] = ws_->hout[1];
-      }
+      if (den_mu) TRY(sync());
     } else {
+      // the merge kernel writes the selection straight into mapped host memory
+      double* dm = ws_->dmap + ws_->oT;
+      const int64_t kc = ws_->kcap;
       TRY(gi::launch_topk(ws_->p, ke, mode, ws_->beta, ws_->g, mu, j_base_, ws_->ckey, ws_->cidx,
-                          ws_->cval, ws_->oidx, ws_->oval, ws_->okey, ws_->ocnt, s,
-                          den_mu ? ws_->scal + 5 : nullptr));
+                          ws_->cval, reinterpret_cast<int64_t*>(dm + 1), dm + 1 + kc,
+                          reinterpret_cast<uint64_t*>(dm + 1 + 2 * kc),
+                          reinterpret_cast<int64_t*>(dm), s, den_mu ? ws_->scal + 5 : nullptr));
       launches += 2;
-      double* ho = ws_->hout;
-      if (den_mu)
-        GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + 3 * ke, ws_->scal + 4, 2 * sizeof(double),
-                                    cudaMemcpyDeviceToHost, s));
-      GI_CUDA_TRY(cudaMemcpyAsync(ho, ws_->ocnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      GI_CUDA_TRY(cudaMemcpyAsync(ho + 1, ws_->oidx, sizeof(int64_t) * ke, cudaMemcpyDeviceToHost,
-                                  s));
-      GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + ke, ws_->oval, sizeof(double) * ke,
-                                  cudaMemcpyDeviceToHost, s));
-      if (sharded())
-        GI_CUDA_TRY(cudaMemcpyAsync(ho + 1 + 2 * ke, ws_->okey, sizeof(uint64_t) * ke,
-                                    cudaMemcpyDeviceToHost, s));
       TRY(sync());
+      const double* ho = ws_->hmap + ws_->oT;
       int64_t cnt = 0;
       memcpy(&cnt, ho, sizeof(int64_t));
       const int64_t* hi = reinterpret_cast<const int64_t*>(ho + 1);
-      const uint64_t* hk = reinterpret_cast<const uint64_t*>(ho + 1 + 2 * ke);
+      const uint64_t* hk = reinterpret_cast<const uint64_t*>(ho + 1 + 2 * kc);
       out.resize((size_t)cnt);
-      for (int64_t t = 0; t < cnt; ++t) out[t] = Pair{hi[t], ho[1 + ke + t]};
+      for (int64_t t = 0; t < cnt; ++t) out[t] = Pair{hi[t], ho[1 + kc + t]};
       if (sharded()) keys.assign(hk, hk + cnt);
-      if (den_mu) {
-        den_mu[0] = ho[1 + 3 * ke];
-        den_mu[1] = ho[2 + 3 * ke];
-      }
+    }
+    if (den_mu) {
+      den_mu[0] = ws_->hmap[ws_->oM];
+      den_mu[1] = ws_->hmap[ws_->oM + 1];
     }
     if (sharded() && ke > 0) TRY(merge_shards(out, keys, ke));
     std::sort(out.begin(), out.end(), [](const Pair& a, const Pair& b) { return a.idx < b.idx; });
@@ -395,10 +398,11 @@ class NativeFit {
     std::vector<double> w;
     local_part(idx_g, w_g, idx, w);
     if (idx.empty()) return 0;
-    TRY(upload_sparse(idx, w, 2));
-    TRY(gi::launch_scatter((int64_t)idx.size(), didx(2), dw(2), ws_->beta, ws_->stream));
-    ++launches;
-    return 0;  // slot 2's staging is not touched again before the refresh's sync
+    // staged now, launched by the next refresh after its single upload
+    TRY(stage(idx.data(), (int64_t)idx.size(), pend_idx_));
+    TRY(stage(w.data(), (int64_t)w.size(), pend_w_));
+    pend_k_ = (int64_t)idx.size();
+    return 0;
   }
 
  private:
@@ -582,8 +586,7 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
         // den = ||X_S g_S + C g_cov||^2 and mu = num / den stay on the device; the
         // first candidate top-k reads mu there, so den, mu and the candidate come
         // back in one sync (iht.py:276-280)
-        TRY(F.image_enqueue(ridx, rg, c ? &gcov : nullptr));
-        TRY(gi::launch_ratio(num, ws->scal, 4, 5, ws->stream));
+        TRY(F.image_enqueue(ridx, rg, c ? &gcov : nullptr, 5, num, ws->dmap + ws->oM));
         double den_mu[2] = {0.0, 0.0};
         TRY(F.topk(1, 0.0, cfg->k, cand, den_mu));
         const double den = den_mu[0];

@@ -221,6 +221,62 @@ __global__ void sumsq_kernel(int64_t m, const double* __restrict__ x, double* __
   }
 }
 
+// Fused image norm of the native loop: scal[slot] = sum_i keep_i (x_i + C_i w)^2
+// -- add_cov, mask and sumsq in one pass, with the same per-element operations
+// (so the same bits).  When ratio_out >= 0 the last block also writes the
+// normalised step scal[ratio_out] = ratio_num / scal[slot] (iht.py:244), and
+// host_out (mapped host memory, may be NULL) receives {scal[slot], ratio}.
+__global__ void image_sumsq_kernel(int64_t m, const double* __restrict__ x,
+                                   const double* __restrict__ C, int c,
+                                   const double* __restrict__ w, const uint8_t* __restrict__ keep,
+                                   double* __restrict__ scal, int slot, int ratio_out,
+                                   double ratio_num, double* __restrict__ host_out, RedWs ws) {
+  __shared__ double sh[32];
+  double acc[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double xi = x[i];
+    if (c > 0) {
+      double cb = 0.0;
+      for (int l = 0; l < c; ++l) cb = __dadd_rn(cb, __dmul_rn(C[i * c + l], w[l]));
+      xi = __dadd_rn(xi, cb);
+    }
+    if (keep && !keep[i]) xi = 0.0;
+    acc[0] += xi * xi;
+  }
+  block_sum<1>(acc, sh);
+  if (threadIdx.x == 0) ws.partials[blockIdx.x] = acc[0];
+  if (last_block(ws.ticket) && threadIdx.x < 32) {
+    const double s = fold_sum(ws.partials, 1, 0, gridDim.x);
+    if (threadIdx.x == 0) {
+      scal[slot] = s;
+      double ratio = 0.0;
+      if (ratio_out >= 0) {
+        ratio = ratio_num / s;
+        scal[ratio_out] = ratio;
+      }
+      if (host_out) {
+        host_out[0] = s;
+        host_out[1] = ratio;
+      }
+      *ws.ticket = 0u;
+    }
+  }
+}
+
+// Copy (or gather, when idx != NULL) up to kMaxPub segments of 8-byte words
+// into `out` -- mapped host memory -- so a phase's results reach the host with
+// one small launch instead of one copy-engine transfer per array.
+__global__ void publish_kernel(PubArgs a, unsigned long long* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int q = 0; q < a.nseg; ++q) {
+    const PubSeg sg = a.seg[q];
+    const unsigned long long* src = static_cast<const unsigned long long*>(sg.src);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < sg.count; t += stride)
+      out[sg.dst + t] = sg.idx ? src[sg.idx[t]] : src[t];
+  }
+}
+
 // out = x + C @ w (length n; C row-major (n, c)); used for X_S w + C w_cov
 __global__ void add_cov_kernel(int64_t n, const double* __restrict__ C, int c,
                                const double* __restrict__ w, double* __restrict__ x) {
@@ -283,6 +339,28 @@ int launch_sumsq(int64_t m, const double* x, double* scal, int slot, double* par
                  unsigned int* ticket, cudaStream_t s) {
   RedWs ws{partials, ticket};
   sumsq_kernel<<<red_grid(m), kRedThreads, 0, s>>>(m, x, scal, slot, ws);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_image_sumsq(int64_t m, const double* x, const double* C, int c, const double* w,
+                       const uint8_t* keep, double* scal, int slot, int ratio_out,
+                       double ratio_num, double* host_out, double* partials,
+                       unsigned int* ticket, cudaStream_t s) {
+  RedWs ws{partials, ticket};
+  image_sumsq_kernel<<<red_grid(m), kRedThreads, 0, s>>>(m, x, C, c, w, keep, scal, slot,
+                                                         ratio_out, ratio_num, host_out, ws);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_publish(const PubArgs& a, void* out, cudaStream_t s) {
+  int64_t most = 0;
+  for (int q = 0; q < a.nseg; ++q) most = a.seg[q].count > most ? a.seg[q].count : most;
+  if (most == 0) return 0;
+  int64_t blocks = (most + 255) / 256;
+  if (blocks > 64) blocks = 64;
+  publish_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, static_cast<unsigned long long*>(out));
   GI_LAUNCH_CHECK();
   return 0;
 }
