@@ -90,6 +90,32 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def smem_roofline(n, p, ms, sm_mhz, sms, missing):
+    """Secondary roofline of aty_fast_kernel: its shared-memory traffic against
+    the SM crossbar (128 B/clk/SM, B300_MICROARCH.md "LDS/STS") at the SM clock
+    sampled during the run.  LSU shared-memory traffic per byte of the tiled
+    matrix: 1 B read back from the TMA-staged block by the consumer warp and
+    4 B of lookup-table read, plus one 128 KiB table build per (work item,
+    sample tile).  The TMA bulk copies fill shared memory through the async
+    copy path, not the LSU crossbar: this count matches ncu's
+    shared-memory LSU wavefronts of the kernel (1.04e9 modelled vs 1.078e9
+    measured at config 3, profiles/r01_summary.md).  Groups with a missing
+    genotype add a second 4 B lookup per byte (not counted here)."""
+    if not ms or not sm_mhz:
+        return None
+    T = (n + 511) // 512
+    G = (p + 31) // 32
+    per_wave = sms * 112  # kMaxGroups groups per work item (aty.cu)
+    items = min(sms * ((G + per_wave - 1) // per_wave), G)
+    smem_bytes = 5 * G * T * 4096 + items * T * 131072
+    achieved = smem_bytes / (ms / 1e3) / 1e9
+    peak = 128 * sms * sm_mhz * 1e6 / 1e9
+    return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "bytes_per_launch": smem_bytes,
+            "peak_basis": f"128 B/clk/SM x {sms} SMs x {sm_mhz:.0f} MHz (median sampled SM clock)",
+            "note": "lower bound when groups carry missing genotypes" if missing else None}
+
+
 def traffic_from_profile(n, p):
     path = os.path.join(ROOT, "profiles", "aty_fast_traffic.json")
     try:
@@ -429,6 +455,7 @@ def main():
             torch.distributed.destroy_process_group()
         return
 
+    clk = clocks.summary()
     # ---- roofline of the X^T r kernel
     n, p_local = a.n, (geno.local.p if sharded else a.p)
     nb = (n + 3) // 4
@@ -463,12 +490,15 @@ def main():
         "xtr_ms": aty_avg,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "aty_fast_kernel", "bytes_per_launch": alg_bytes},
+                     "kernel": "aty_fast_kernel", "bytes_per_launch": alg_bytes,
+                     "smem": smem_roofline(n, p_local, aty_avg, clk.get("sm_mhz"),
+                                           torch.cuda.get_device_properties(local)
+                                           .multi_processor_count, a.missing)},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h // max(a.steps, 1)},
         "gpu_launches": launches,
-        "clocks": clocks.summary(),
+        "clocks": clk,
     }
     print(json.dumps(line), flush=True)
     if sharded:

@@ -18,6 +18,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -185,8 +188,14 @@ class NativeFit {
     }
     return 0;
   }
+  double sync_us = 0.0;
+  int syncs = 0;
   int sync() {
+    const auto t0 = std::chrono::steady_clock::now();
     GI_CUDA_TRY(cudaStreamSynchronize(ws_->stream));
+    sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+                   .count();
+    ++syncs;
     ws_->in_off = ws_->in_flushed = 0;  // every staged copy has landed
     return 0;
   }
@@ -710,6 +719,9 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   res->iterations = iterations;
   res->reason = reason;
   res->backtracks = total_bt;
+  if (getenv("GI_TRACE_FIT"))
+    fprintf(stderr, "gi_fit: %lld iterations, %d syncs, %.1f us waiting in sync, %d launches\n",
+            (long long)iterations, F.syncs, F.sync_us, F.launches);
   res->kernel_launches = F.launches;
   res->aty_ms_total = F.aty_ms;
   res->aty_launches = F.aty_launches;

@@ -1,0 +1,7 @@
+cd "$GRAFT_REPO_ROOT"; export PYTHONPATH="$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+for c in c2 c1; do
+  timeout 120 python tools/small_fits.py $c || exit 1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/small_$c.csv python tools/small_fits.py $c > /dev/null 2>&1
+done
+ls -la gpurun_out
