@@ -23,7 +23,7 @@ void gi_set_error(const char* fmt, ...) {
 }
 
 static int matrix_shell(int64_t n, int64_t p, int device, gi_matrix** out,
-                        std::unique_ptr<gi_matrix>& h) {
+                        std::unique_ptr<gi_matrix>& h, bool zero_tiles = true) {
   CHECK_ARG(out != nullptr, "output handle pointer is NULL");
   CHECK_ARG(n >= 0 && p >= 0, "matrix dimensions must be non-negative");
   int count = 0;
@@ -39,7 +39,7 @@ static int matrix_shell(int64_t n, int64_t p, int device, gi_matrix** out,
   h->G = (p + GI_GROUP - 1) / GI_GROUP;
   GI_CUDA_TRY(cudaSetDevice(device));
   GI_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-  TRY(alloc(h->x, (size_t)(h->T * h->G) * GI_BLOCK_BYTES, device, true));
+  TRY(alloc(h->x, (size_t)(h->T * h->G) * GI_BLOCK_BYTES, device, zero_tiles));
   TRY(alloc(h->u, sizeof(double) * p, device, true));
   TRY(alloc(h->v, sizeof(double) * p, device, true));
   TRY(alloc(h->miss_cnt, sizeof(int32_t) * p, device, true));
@@ -176,7 +176,6 @@ int gi_matrix_with_stats(const gi_matrix* src, const double* u, const double* v,
   h->miss_cnt = src->miss_cnt;
   h->gmiss = src->gmiss;
   h->s1cnt = src->s1cnt;
-  h->fit_pool = src->fit_pool;
   DeviceGuard g(h->device);
   GI_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   TRY(alloc(h->u, sizeof(double) * h->p, h->device, false));
@@ -192,7 +191,8 @@ int gi_matrix_subset_rows(const gi_matrix* src, const int64_t* rows, int64_t m, 
   for (int64_t i = 0; i < m; ++i)
     CHECK_ARG(rows[i] >= 0 && rows[i] < src->n, "row index out of range");
   std::unique_ptr<gi_matrix> h;
-  TRY(matrix_shell(m, src->p, src->device, out, h));
+  // the gather kernel writes every word of every block (padding codes as 0)
+  TRY(matrix_shell(m, src->p, src->device, out, h, m == 0 || src->p == 0));
   DeviceGuard g(src->device);
   if (m > 0 && src->p > 0) {
     std::shared_ptr<DevMem> drows;

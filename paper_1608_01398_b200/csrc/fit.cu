@@ -18,6 +18,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -55,6 +57,7 @@ struct FitWs {
   int64_t oR = 0, oT = 0, oM = 0, oS = 0;  // regions: refresh, top-k, den/mu, image
   std::vector<void*> dev_allocs;
   bool primed = false, masked = false;
+  uint64_t primed_uid = 0;  // handle whose inputs are resident (y == NULL calls)
   double n_eff = 0.0;
 
   ~FitWs() {
@@ -80,6 +83,23 @@ struct FitWs {
     return 0;
   }
 };
+
+// Process-wide workspace pool per device.  Deliberately never destroyed: it
+// would otherwise be torn down after the CUDA runtime at process exit.
+struct FitPool {
+  std::mutex mu;
+  std::vector<std::shared_ptr<FitWs>> items;
+};
+constexpr size_t kPoolCap = 32;
+
+FitPool& fit_pool_for(int device) {
+  static std::mutex mu;
+  static std::map<int, FitPool*>* pools = new std::map<int, FitPool*>();
+  std::lock_guard<std::mutex> lock(mu);
+  FitPool*& pool = (*pools)[device];
+  if (!pool) pool = new FitPool();
+  return *pool;
+}
 
 int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) {
   auto ws = std::make_shared<FitWs>();
@@ -452,16 +472,17 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   DeviceGuard guard(h->device);
   const int64_t kcap = std::max<int64_t>(std::max<int64_t>(cfg->k, warm_k), 1);
 
-  // take a workspace of the right shape from the handle's pool (or make one);
-  // y == NULL (resident inputs) needs one primed by an earlier call
+  // take a workspace of the right shape from the device's pool (or make one);
+  // y == NULL (resident inputs) needs one primed by an earlier call on h
+  FitPool& pool = fit_pool_for(h->device);
   std::shared_ptr<FitWs> ws;
   {
-    std::lock_guard<std::mutex> lock(h->fit_pool->mu);
-    auto& items = h->fit_pool->items;
-    for (size_t i = 0; i < items.size(); ++i) {
-      auto cand = std::static_pointer_cast<FitWs>(items[i]);
+    std::lock_guard<std::mutex> lock(pool.mu);
+    auto& items = pool.items;
+    for (size_t i = items.size(); i-- > 0;) {  // most recently returned first
+      const auto& cand = items[i];
       if (cand->c == c && cand->kcap >= kcap && cand->n == h->n && cand->p == h->p &&
-          (y != nullptr || cand->primed)) {
+          (y != nullptr || (cand->primed && cand->primed_uid == h->uid))) {
         ws = cand;
         items.erase(items.begin() + (long)i);
         break;
@@ -473,13 +494,18 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
     TRY(make_ws(h, c, kcap, ws));
   }
   struct PoolReturn {
-    std::shared_ptr<gi_matrix::FitPool> pool;
+    FitPool& pool;
     std::shared_ptr<FitWs> ws;
     ~PoolReturn() {
-      std::lock_guard<std::mutex> lock(pool->mu);
-      pool->items.push_back(ws);
+      std::shared_ptr<FitWs> evicted;  // released outside the lock
+      std::lock_guard<std::mutex> lock(pool.mu);
+      pool.items.push_back(ws);
+      if (pool.items.size() > kPoolCap) {
+        evicted = pool.items.front();
+        pool.items.erase(pool.items.begin());
+      }
     }
-  } pool_return{h->fit_pool, ws};
+  } pool_return{pool, ws};
   cudaStream_t s = ws->stream;
   const int64_t n = h->n, p = h->p;
   double n_eff = (double)n;
@@ -523,6 +549,7 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   GI_CUDA_TRY(cudaMemsetAsync(ws->beta, 0, sizeof(double) * std::max<int64_t>(p, 1), s));
   GI_CUDA_TRY(cudaStreamSynchronize(s));
   ws->primed = true;
+  ws->primed_uid = h->uid;
   ws->masked = masked;
   ws->n_eff = n_eff;
   }

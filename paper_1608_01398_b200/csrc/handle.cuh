@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -33,11 +34,31 @@ struct DevMem {
       int prev = 0;
       cudaGetDevice(&prev);
       cudaSetDevice(device);
-      cudaFree(ptr);
+      // like cudaFree: no stream may still be using the buffer; the bytes then
+      // go back to the device pool (kept mapped, see device_pool) for reuse
+      cudaDeviceSynchronize();
+      cudaFreeAsync(ptr, 0);
       cudaSetDevice(prev);
     }
   }
 };
+
+// The device's default stream-ordered pool, set to keep freed memory mapped:
+// CV fold copies and fit workspaces are allocated and dropped repeatedly, and
+// re-mapping gigabytes through cudaMalloc/cudaFree costs milliseconds each.
+inline cudaMemPool_t device_pool(int device) {
+  static std::mutex mu;
+  static bool configured[64] = {};
+  cudaMemPool_t pool = nullptr;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (device >= 0 && device < 64 && !configured[device]) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    configured[device] = true;
+  }
+  return pool;
+}
 
 struct DeviceGuard {
   int prev = 0;
@@ -48,12 +69,25 @@ struct DeviceGuard {
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
+// Device buffer from the pool, usable from any stream on return.
 inline int alloc(std::shared_ptr<DevMem>& out, size_t bytes, int device, bool zero) {
   out = std::make_shared<DevMem>();
   out->device = device;
   if (bytes == 0) bytes = 16;
-  GI_CUDA_TRY(cudaMalloc(&out->ptr, bytes));
-  if (zero) GI_CUDA_TRY(cudaMemset(out->ptr, 0, bytes));
+  cudaMemPool_t pool = device_pool(device);
+  cudaError_t e = cudaMallocAsync(&out->ptr, bytes, 0);
+  if (e == cudaErrorMemoryAllocation && pool) {  // give back cached bytes, retry once
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(&out->ptr, bytes, 0);
+  }
+  if (e != cudaSuccess) {
+    out->ptr = nullptr;
+    GI_CUDA_TRY(e);
+  }
+  if (zero) GI_CUDA_TRY(cudaMemsetAsync(out->ptr, 0, bytes, 0));
+  GI_CUDA_TRY(cudaStreamSynchronize(0));
   return 0;
 }
 
@@ -94,14 +128,15 @@ struct gi_matrix {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   Scratch s_a, s_b, s_c, s_d;
-  // workspaces of the native fit loop (fit.cu): a pool, so independent fits on
-  // one matrix run concurrently, each on its own stream.  Shared with the
-  // with_stats copies (a workspace depends on the shape, not on the stats).
-  struct FitPool {
-    std::mutex mu;
-    std::vector<std::shared_ptr<void>> items;
-  };
-  std::shared_ptr<FitPool> fit_pool = std::make_shared<FitPool>();
+  // Identity of this handle.  The native fit loop's workspaces (fit.cu) live
+  // in a process-wide pool per device keyed by shape, so fits on any matrix of
+  // that shape (CV fold copies, with_stats copies) reuse them; the uid tells
+  // the resident-input path which handle primed a workspace.
+  uint64_t uid = next_uid();
+  static uint64_t next_uid() {
+    static std::atomic<uint64_t> counter{0};
+    return ++counter;
+  }
 
   gi::MatrixDesc desc() const {
     gi::MatrixDesc d;

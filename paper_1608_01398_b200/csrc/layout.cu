@@ -5,6 +5,8 @@
 //   PackedGenotypeMatrix.from_bed_buffer  geno_matrix.py:281-292 (bytes kept verbatim)
 //   _stats_kernel / _packed_stats         geno_matrix.py:106-139, :239-246
 //   random_packed_matrix                  simulate.py:56-65 (same law, hash-based stream)
+#include <climits>
+
 #include "common.cuh"
 
 namespace gi {
@@ -223,34 +225,79 @@ int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_
 }
 
 // ---------------------------------------------------------------- subset rows
-// dst holds m samples: sample i of dst = sample rows[i] of src.  One thread per
-// (SNP, dst word).  Padding codes past m stay zero.
-__global__ void subset_rows_kernel(MatrixDesc src, MatrixDesc dst, uint8_t* __restrict__ x,
-                                   const int64_t* __restrict__ rows) {
-  const int64_t words = dst.T * GI_TILE_WORDS;
-  const int64_t total = dst.p * words;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / words;
-    const int64_t wg = e - j * words;
-    uint32_t word = 0;
-    for (int s = 0; s < 16; ++s) {
-      const int64_t i = wg * 16 + s;
-      if (i >= dst.n) break;
-      const int64_t si = rows[i];
+// dst holds m samples: sample i of dst = sample rows[i] of src.  One CTA per
+// (dst tile, SNP group), 8 warps.  Warp w builds rows q = w, w + 8, ... of the
+// dst block; lane L assembles word q ^ L of SNP 32 g + L, so every store is
+// one coalesced 128-B row.  When the tile's source samples lie in at most
+// kSubStage consecutive source tiles (sorted rows, as for CV folds) those
+// blocks are staged in shared memory with 16-B loads; the gather of a code
+// then reads byte (L ^ sw) * 128 + 4 L + .. of a staged block -- bank L, so
+// conflict-free.  Other row sets read the source blocks from global memory.
+// The source index of dst sample 16 w' + s is kept at srow[s * 32 + w'], so
+// the 32 lanes (w' = q ^ L) read 32 distinct banks.  Padding codes stay zero.
+constexpr int kSubStage = 8;
+
+__global__ void __launch_bounds__(256) subset_rows_kernel(MatrixDesc src, MatrixDesc dst,
+                                                          uint8_t* __restrict__ x,
+                                                          const int64_t* __restrict__ rows) {
+  __shared__ __align__(16) uint8_t stage[kSubStage * GI_BLOCK_BYTES];
+  __shared__ int32_t srow[GI_TILE_SAMPLES];
+  __shared__ int s_lo, s_hi;
+  const int64_t tp = blockIdx.x / dst.G;
+  const int64_t g = blockIdx.x - tp * dst.G;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_lo = INT_MAX;
+    s_hi = -1;
+  }
+  __syncthreads();
+  for (int e = tid; e < GI_TILE_SAMPLES; e += blockDim.x) {
+    const int64_t i = tp * GI_TILE_SAMPLES + e;
+    int32_t si = -1;
+    if (i < dst.n) {
+      si = (int32_t)rows[i];
       GI_ASSERT(si >= 0 && si < src.n);
-      const uint32_t sw = *reinterpret_cast<const uint32_t*>(
-          src.x + word_offset_chk(src, si >> 9, j, (int)((si >> 4) & 31)));
-      word |= ((sw >> (2 * (si & 15))) & 3u) << (2 * s);
+      atomicMin(&s_lo, si >> 9);
+      atomicMax(&s_hi, si >> 9);
     }
-    *reinterpret_cast<uint32_t*>(x + word_offset_chk(dst, wg >> 5, j, (int)(wg & 31))) = word;
+    srow[(e & 15) * 32 + (e >> 4)] = si;
+  }
+  __syncthreads();
+  const int lo = s_lo;
+  const bool staged = s_hi >= 0 && s_hi - lo < kSubStage;
+  if (staged) {
+    const int nblk = s_hi - lo + 1;
+    for (int e = tid; e < nblk * (GI_BLOCK_BYTES / 16); e += blockDim.x) {
+      const int b = e / (GI_BLOCK_BYTES / 16), o = e - b * (GI_BLOCK_BYTES / 16);
+      reinterpret_cast<uint4*>(stage)[e] = __ldg(
+          reinterpret_cast<const uint4*>(src.x + block_offset(lo + b, g, src.G)) + o);
+    }
+  }
+  __syncthreads();
+  const int warp = tid >> 5, L = tid & 31;
+  uint8_t* out = x + block_offset(tp, g, dst.G);
+  for (int q = warp; q < 32; q += 8) {
+    const int wq = q ^ L;
+    uint32_t word = 0;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int32_t si = srow[s * 32 + wq];
+      if (si >= 0) {
+        const int off = (((L ^ ((si >> 4) & 31))) << 7) + (L << 2) + ((si >> 2) & 3);
+        const uint32_t b = staged ? stage[((si >> 9) - lo) * GI_BLOCK_BYTES + off]
+                                  : __ldg(src.x + block_offset(si >> 9, g, src.G) + off);
+        word |= ((b >> (2 * (si & 3))) & 3u) << (2 * s);
+      }
+    }
+    *reinterpret_cast<uint32_t*>(out + (q << 7) + (L << 2)) = word;
   }
 }
 
 int launch_subset_rows(const MatrixDesc& src, const MatrixDesc& dst, uint8_t* x,
                        const int64_t* d_rows, cudaStream_t s) {
   if (dst.p == 0 || dst.n == 0) return 0;
-  subset_rows_kernel<<<grid_for(dst.p * dst.T * 32, 256), 256, 0, s>>>(src, dst, x, d_rows);
+  const int64_t blocks = dst.T * dst.G;
+  subset_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(src, dst, x, d_rows);
   GI_LAUNCH_CHECK();
   return 0;
 }

@@ -183,3 +183,27 @@ def test_many_covariates_and_budget_above_p(native):
         got = gi.fit(view, y, gi.IhtConfig(k=k), native=native)
         _assert_fit(got, want.support, want.weights, want.covar, want.loss_trace,
                     want.iterations, want.reason)
+
+
+@pytest.mark.parametrize("std_mode", ["train", "global"])
+def test_cv_compact_folds_match_masked_folds(std_mode, monkeypatch):
+    """Training folds as compact device copies (subset_rows) or as row masks
+    over the resident matrix: same k_best, per-fold MSE grid and final model
+    (the fast X^T r tiles the rows differently, hence 1e-6, not bits)."""
+    gi = _gi()
+    codes = oracle.random_codes(700, 900, seed=31, missing_rate=0.02)
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=700))
+    rng = np.random.default_rng(5)
+    support = np.sort(rng.choice(900, 6, replace=False))
+    y = m.ax_columns(support, rng.standard_normal(6)) + rng.normal(0, 0.3, 700)
+    plan = gi.CvPlan.build(700, 4, np.arange(1, 10), seed=11)
+    reports = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("GI_CV_COMPACT", mode)
+        reports[mode] = gi.cv_iht(view, y, plan, gi.IhtConfig(k=9), std_mode=std_mode)
+    a, b = reports["0"], reports["1"]
+    assert a.k_best == b.k_best
+    np.testing.assert_allclose(b.mse, a.mse, rtol=1e-6)
+    np.testing.assert_array_equal(b.final_model.support, a.final_model.support)
+    np.testing.assert_allclose(b.final_model.weights, a.final_model.weights, rtol=1e-6)

@@ -146,3 +146,28 @@ def test_bed_roundtrip_and_shards(tmp_path):
     bad.write_bytes(bytes([0x6C, 0x1B, 0x01]) + bytes(3))
     with pytest.raises(gi.PlinkFormatError, match="BED disagrees"):
         gi.read_bed(bad, 4, 4)
+
+
+@pytest.mark.parametrize("order", ["sorted", "shuffled", "duplicates", "spread"])
+def test_subset_rows_any_row_order(order):
+    """Device row gather vs codes[rows]: sorted rows (staged source tiles),
+    unsorted / duplicated / widely spread rows (global-memory fallback), with
+    missing codes, a ragged last tile and a ragged last SNP group."""
+    gi = _gm()
+    rng = np.random.default_rng(7)
+    n, p = 5000, 77
+    codes = oracle.random_codes(n, p, seed=3, missing_rate=0.05)
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    if order == "sorted":
+        rows = np.sort(rng.choice(n, 3001, replace=False))
+    elif order == "shuffled":
+        rows = rng.permutation(n)[:2999]
+    elif order == "duplicates":
+        rows = rng.integers(0, n, 1500)
+    else:
+        rows = np.concatenate([np.arange(0, 4800, 9), [n - 1, 0, n - 2]])
+    sub = m.subset_rows(rows)
+    np.testing.assert_array_equal(sub.to_codes(), codes[rows])
+    ref = oracle.OraclePacked.from_codes(codes[rows])
+    np.testing.assert_array_equal(sub.u, ref.u)
+    np.testing.assert_array_equal(sub.v, ref.v)

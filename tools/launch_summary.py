@@ -13,7 +13,7 @@ for r in csv.DictReader(lines):
         continue
     unit = r["Metric Unit"]
     v = float(r["Metric Value"].replace(",", ""))
-    us = v / 1e3 if unit == "nsecond" else v if unit == "usecond" else v * 1e3
+    us = v / 1e3 if unit in ("nsecond", "ns") else v if unit in ("usecond", "us") else v * 1e3
     rows.append((r["Kernel Name"].split("(")[0].split("<")[0], us))
 if tail:
     rows = rows[-tail:]
