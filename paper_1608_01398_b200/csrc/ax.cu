@@ -37,40 +37,43 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
     terms[t][3] = __dsub_rn(__dmul_rn(2.0, scale), shift);  // code 11: dose 2
   }
   __syncthreads();
-  const int64_t words = (m.n + 15) / 16;
-  for (int64_t wg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; wg < words;
-       wg += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i0 = wg * 16;
-    const int cnt = (int)((m.n - i0) < 16 ? (m.n - i0) : 16);
-    double acc[16];
+  // one thread per packed byte (4 samples): at the small n of path and CV fits
+  // a thread per 16-sample word left most SMs idle.  Each sample still adds the
+  // columns' terms in the caller's order (same bits as _ax_cols_kernel).
+  const int64_t nbytes = (m.n + 3) / 4;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbytes;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = b * 4;
+    const int cnt = (int)((m.n - i0) < 4 ? (m.n - i0) : 4);
+    double acc[4];
 #pragma unroll
-    for (int s = 0; s < 16; ++s) acc[s] = (accumulate && s < cnt) ? out[i0 + s] : 0.0;
-    const int64_t tile = wg >> 5;
-    const int wp = (int)(wg & 31);
-    // columns in batches of 8: issue the 8 independent word loads first, then
-    // accumulate in the caller's column order (same per-sample add sequence)
+    for (int s = 0; s < 4; ++s) acc[s] = (accumulate && s < cnt) ? out[i0 + s] : 0.0;
+    const int64_t tile = b >> 7;
+    const int wp = (int)((b >> 2) & 31);
+    const int bo = (int)(b & 3);
+    // columns in batches of 8: issue the 8 independent byte loads first, then
+    // accumulate in the caller's column order
     for (int t0 = 0; t0 < k; t0 += 8) {
-      uint32_t words[8];
+      uint32_t bytes[8];
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const int t = t0 + b;
-        words[b] = (t < k && live[t])
-                       ? __ldg(reinterpret_cast<const uint32_t*>(
-                             m.x + word_offset_chk(m, tile, cols[t], wp)))
+      for (int q = 0; q < 8; ++q) {
+        const int t = t0 + q;
+        bytes[q] = (t < k && live[t])
+                       ? (uint32_t)__ldg(m.x + word_offset_chk(m, tile, cols[t], wp) + bo)
                        : 0u;
       }
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const int t = t0 + b;
+      for (int q = 0; q < 8; ++q) {
+        const int t = t0 + q;
         if (t < k && live[t]) {
 #pragma unroll
-          for (int s = 0; s < 16; ++s)
-            acc[s] = __dadd_rn(acc[s], terms[t][(words[b] >> (2 * s)) & 3u]);
+          for (int s = 0; s < 4; ++s)
+            acc[s] = __dadd_rn(acc[s], terms[t][(bytes[q] >> (2 * s)) & 3u]);
         }
       }
     }
 #pragma unroll
-    for (int s = 0; s < 16; ++s)
+    for (int s = 0; s < 4; ++s)
       if (s < cnt) out[i0 + s] = acc[s];
   }
 }
@@ -78,9 +81,9 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
 int launch_ax(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
               const double* w, int64_t k, double* out, int accumulate, cudaStream_t s) {
   if (m.n == 0) return 0;
-  const int64_t words = (m.n + 15) / 16;
+  const int64_t nbytes = (m.n + 3) / 4;
   const int threads = 128;
-  int64_t blocks = (words + threads - 1) / threads;
+  int64_t blocks = (nbytes + threads - 1) / threads;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (k <= 0) {
     if (!accumulate) GI_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * m.n, s));

@@ -367,8 +367,9 @@ class NativeFit {
       TRY(gi::launch_topk(ws_->p, ke, mode, ws_->beta, ws_->g, mu, j_base_, ws_->ckey, ws_->cidx,
                           ws_->cval, reinterpret_cast<int64_t*>(dm + 1), dm + 1 + kc,
                           reinterpret_cast<uint64_t*>(dm + 1 + 2 * kc),
-                          reinterpret_cast<int64_t*>(dm), s, den_mu ? ws_->scal + 5 : nullptr));
-      launches += 2;
+                          reinterpret_cast<int64_t*>(dm), s, den_mu ? ws_->scal + 5 : nullptr,
+                          ws_->ticket));
+      launches += 1;
       TRY(sync());
       const double* ho = ws_->hmap + ws_->oT;
       int64_t cnt = 0;

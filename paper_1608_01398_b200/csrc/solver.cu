@@ -382,14 +382,24 @@ int launch_add_cov(int64_t n, const double* C, int c, const double* w, double* x
 constexpr int kTopkChunk = 4096;
 constexpr int kTopkThreads = 512;
 
+// Shared-memory state of one block-wide select, declared once per kernel
+// (static __shared__ inside the templates would be duplicated per Get type).
+struct SelShared {
+  unsigned int hist[256];
+  uint64_t s_key, s_kmask;
+  uint32_t s_sec, s_smask;
+  int64_t s_kk;
+  int s_done;
+};
+
 template <typename Get>
 __device__ void block_select(int64_t m, int64_t k, Get get, uint64_t& thr_key,
-                             uint32_t& thr_sec) {
-  __shared__ unsigned int hist[256];
-  __shared__ uint64_t s_key, s_kmask;
-  __shared__ uint32_t s_sec, s_smask;
-  __shared__ int64_t s_kk;
-  __shared__ int s_done;
+                             uint32_t& thr_sec, SelShared& sh) {
+  unsigned int* hist = sh.hist;
+  uint64_t &s_key = sh.s_key, &s_kmask = sh.s_kmask;
+  uint32_t &s_sec = sh.s_sec, &s_smask = sh.s_smask;
+  int64_t& s_kk = sh.s_kk;
+  int& s_done = sh.s_done;
   if (threadIdx.x == 0) {
     s_key = 0;
     s_kmask = 0;
@@ -468,6 +478,7 @@ __device__ __forceinline__ bool ge_thr(uint64_t key, uint32_t sec, uint64_t tk, 
   return key > tk || (key == tk && sec >= ts);
 }
 
+
 // mode 0: value = g_j; mode 1: value = beta_j - mu * g_j.  key = |value|.
 __device__ __forceinline__ double topk_value(int mode, const double* beta, const double* g,
                                              double mu, int64_t j) {
@@ -479,15 +490,68 @@ __device__ __forceinline__ uint64_t key_of(double val) {
   return (uint64_t)__double_as_longlong(fabs(val)) + 1ull;
 }
 
+// Exact top-k over `mc` candidates -> out (unordered) + count, by one block.
+// kL2: read the candidates through L2 only (ld.global.cg) -- they were written
+// by other blocks of the same launch (the fused form below).
+template <bool kL2>
+__device__ void topk_merge_body(int64_t mc, int64_t k, const uint64_t* cand_key,
+                                const int64_t* cand_idx, const double* cand_val,
+                                int64_t* out_idx, double* out_val, uint64_t* out_key,
+                                int64_t* out_count, SelShared& sh) {
+  __shared__ unsigned int s_pos;
+  if (threadIdx.x == 0) s_pos = 0u;
+  __syncthreads();
+  auto key_at = [&](int64_t i) -> uint64_t {
+    return kL2 ? (uint64_t)__ldcg(reinterpret_cast<const unsigned long long*>(cand_key) + i)
+               : cand_key[i];
+  };
+  auto idx_at = [&](int64_t i) -> int64_t {
+    return kL2 ? (int64_t)__ldcg(reinterpret_cast<const long long*>(cand_idx) + i)
+               : cand_idx[i];
+  };
+  auto get = [&](int64_t i, uint64_t& key, uint32_t& sec) {
+    key = key_at(i);
+    sec = ~(uint32_t)idx_at(i);
+  };
+  uint64_t tk;
+  uint32_t ts;
+  block_select(mc, k, get, tk, ts, sh);
+  if (tk == 0) tk = 1;  // never take empty slots
+  for (int64_t i = threadIdx.x; i < mc; i += blockDim.x) {
+    uint64_t key;
+    uint32_t sec;
+    get(i, key, sec);
+    if (ge_thr(key, sec, tk, ts)) {
+      const unsigned pos = atomicAdd(&s_pos, 1u);
+      if (pos < k) {
+        out_idx[pos] = idx_at(i);
+        out_val[pos] = kL2 ? __ldcg(cand_val + i) : cand_val[i];
+        if (out_key) out_key[pos] = key;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *out_count = s_pos < k ? (int64_t)s_pos : k;
+}
+
+struct MergeOut {
+  unsigned int* ticket;  // NULL: the merge runs as its own kernel
+  int64_t* idx;
+  double* val;
+  uint64_t* key;
+  int64_t* count;
+};
+
 // One block per chunk of kTopkChunk elements; writes k candidate slots
 // (cand_key = 0 marks an unused slot).
 __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(
     int64_t p, int64_t k, int mode, const double* __restrict__ beta,
     const double* __restrict__ g, double mu_host, const double* __restrict__ mu_dev,
     int64_t idx_base, uint64_t* __restrict__ cand_key,
-    int64_t* __restrict__ cand_idx, double* __restrict__ cand_val) {
+    int64_t* __restrict__ cand_idx, double* __restrict__ cand_val, MergeOut mo) {
   __shared__ uint64_t keys[kTopkChunk];
   __shared__ unsigned int s_pos;
+  __shared__ SelShared sel;
   const double mu = mu_dev ? *mu_dev : mu_host;
   const int64_t lo = (int64_t)blockIdx.x * kTopkChunk;
   const int64_t hi = lo + kTopkChunk < p ? lo + kTopkChunk : p;
@@ -504,7 +568,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(
   };
   const int64_t kk = k < m ? k : m;
   if (kk < m) {
-    block_select(m, kk, get, tk, ts);
+    block_select(m, kk, get, tk, ts, sel);
   } else {
     tk = 1;
     ts = 0;  // take everything
@@ -530,40 +594,30 @@ __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(
     oi[s] = -1;
     ov[s] = 0.0;
   }
+  // fused merge: the last block to finish selects over all blocks' candidates
+  if (mo.ticket) {
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(mo.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (is_last) {
+      __threadfence();
+      topk_merge_body<true>((int64_t)gridDim.x * k, k, cand_key, cand_idx, cand_val, mo.idx,
+                            mo.val, mo.key, mo.count, sel);
+      if (threadIdx.x == 0) *mo.ticket = 0u;
+    }
+  }
 }
 
-// Single block: exact top-k over `mc` candidates -> out (unordered) + count.
-__global__ void __launch_bounds__(1024) topk_merge_kernel(
+__global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(
     int64_t mc, int64_t k, const uint64_t* __restrict__ cand_key,
     const int64_t* __restrict__ cand_idx, const double* __restrict__ cand_val,
     int64_t* __restrict__ out_idx, double* __restrict__ out_val, uint64_t* __restrict__ out_key,
     int64_t* __restrict__ out_count) {
-  __shared__ unsigned int s_pos;
-  if (threadIdx.x == 0) s_pos = 0u;
-  __syncthreads();
-  auto get = [&](int64_t i, uint64_t& key, uint32_t& sec) {
-    key = cand_key[i];
-    sec = ~(uint32_t)cand_idx[i];
-  };
-  uint64_t tk;
-  uint32_t ts;
-  block_select(mc, k, get, tk, ts);
-  if (tk == 0) tk = 1;  // never take empty slots
-  for (int64_t i = threadIdx.x; i < mc; i += blockDim.x) {
-    uint64_t key;
-    uint32_t sec;
-    get(i, key, sec);
-    if (ge_thr(key, sec, tk, ts)) {
-      const unsigned pos = atomicAdd(&s_pos, 1u);
-      if (pos < k) {
-        out_idx[pos] = cand_idx[i];
-        out_val[pos] = cand_val[i];
-        if (out_key) out_key[pos] = key;
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) *out_count = s_pos < k ? (int64_t)s_pos : k;
+  __shared__ SelShared sel;
+  topk_merge_body<false>(mc, k, cand_key, cand_idx, cand_val, out_idx, out_val, out_key,
+                         out_count, sel);
 }
 
 int64_t topk_blocks(int64_t p) { return (p + kTopkChunk - 1) / kTopkChunk; }
@@ -571,19 +625,24 @@ int64_t topk_blocks(int64_t p) { return (p + kTopkChunk - 1) / kTopkChunk; }
 int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double* g, double mu,
                 int64_t idx_base, uint64_t* cand_key, int64_t* cand_idx, double* cand_val,
                 int64_t* out_idx, double* out_val, uint64_t* out_key, int64_t* out_count,
-                cudaStream_t s, const double* mu_dev) {
+                cudaStream_t s, const double* mu_dev, unsigned int* ticket) {
   if (k <= 0 || p <= 0) {
     GI_CUDA_TRY(cudaMemsetAsync(out_count, 0, sizeof(int64_t), s));
     return 0;
   }
   const int64_t nb = topk_blocks(p);
+  // with a ticket (zero on entry, zero again on exit) the merge runs in the
+  // last local block: one launch instead of two
+  const MergeOut mo{ticket, out_idx, out_val, out_key, out_count};
   topk_local_kernel<<<(unsigned)nb, kTopkThreads, 0, s>>>(p, k, mode, beta, g, mu, mu_dev,
-                                                          idx_base,
-                                                          cand_key, cand_idx, cand_val);
+                                                          idx_base, cand_key, cand_idx, cand_val,
+                                                          mo);
   GI_LAUNCH_CHECK();
-  topk_merge_kernel<<<1, 1024, 0, s>>>(nb * k, k, cand_key, cand_idx, cand_val, out_idx,
-                                       out_val, out_key, out_count);
-  GI_LAUNCH_CHECK();
+  if (!ticket) {
+    topk_merge_kernel<<<1, kTopkThreads, 0, s>>>(nb * k, k, cand_key, cand_idx, cand_val, out_idx,
+                                         out_val, out_key, out_count);
+    GI_LAUNCH_CHECK();
+  }
   return 0;
 }
 
