@@ -247,6 +247,7 @@ def secondary(a):
     import torch
 
     import paper_1608_01398_b200 as gi
+    from paper_1608_01398_b200 import model_select as ms_mod
     from paper_1608_01398_b200.simulate import SimulationSpec, simulate_phenotype
 
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -317,7 +318,10 @@ def secondary(a):
         rep = out
         line["config"] = {"workload": f"BASELINE config 4: n={n} x p={p}, 5-fold CV over "
                                       f"k=1..20 + final fit and refit, k_true={k_true}, "
-                                      f"fold seed 2016", "step": "one cv_iht call"}
+                                      f"fold seed 2016", "step": "one cv_iht call",
+                          "folds": ("compact device copies of the training rows"
+                                    if ms_mod._compact_folds(m, 5) else
+                                    "row masks over the resident matrix")}
         line["value"] = None
         line["cv_seconds"] = ms / 1e3
         line["k_best"] = int(rep.k_best)
