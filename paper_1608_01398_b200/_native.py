@@ -73,6 +73,7 @@ def _declare(lib):
         "gi_matrix_device_stats": ([P, P, P], c_int),
         "gi_matrix_masked_stats": ([P, P, P, P], c_int),
         "gi_aty": ([P, P, c_dbl, P, c_int], c_int),
+        "gi_aty_batched": ([P, P, P, P, P, c_i64, P, c_int], c_int),
         "gi_ax_cols": ([P, P, P, c_i64, P], c_int),
         "gi_decompress": ([P, P, c_i64, P], c_int),
         "gi_dev_ax": ([P, P, P, P, P, c_i64, P, c_int, P], c_int),

@@ -298,11 +298,10 @@ int gi_matrix_masked_stats(const gi_matrix* hc, const uint8_t* keep, double* u, 
 }
 
 // ------------------------------------------------------- host-buffer operators
-int gi_aty(gi_matrix* h, const double* r, double sum_r, double* out, int mode) {
-  CHECK_ARG(h && r && out, "NULL argument");
-  if (h->p == 0) return 0;
-  std::lock_guard<std::mutex> lock(h->mu);
-  DeviceGuard g(h->device);
+// One aty_genetic sweep on h's stream (caller holds h->mu and the device):
+// r, out on the host; u, v device pointers (the handle's or caller stats).
+static int aty_enqueue(gi_matrix* h, const double* r, double sum_r, const double* du,
+                       const double* dv, double* out, int mode) {
   const int64_t npad = h->T * GI_TILE_SAMPLES;
   // scratch layout: s_a = r (fp64 padded) | rt (fp32 padded); s_b = out; s_c = scalars/partials
   TRY(h->s_a.ensure(sizeof(double) * npad + sizeof(float) * npad + 64, h->device));
@@ -317,20 +316,57 @@ int gi_aty(gi_matrix* h, const double* r, double sum_r, double* out, int mode) {
   GI_CUDA_TRY(cudaMemcpyAsync(dr, r, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
   if (mode == 0) {
     GI_CUDA_TRY(cudaMemcpyAsync(scal, &sum_r, sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    TRY(gi::launch_aty_exact(h->desc(), dr, h->du(), h->dv(), scal, 1.0, h->s_b.as<double>(),
-                             h->stream));
+    TRY(gi::launch_aty_exact(h->desc(), dr, du, dv, scal, 1.0, h->s_b.as<double>(), h->stream));
   } else {
     GI_CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), h->stream));
     // mean over the n real samples, then centred fp32 copy and its sum
     TRY(gi::launch_residual(h->n, dr, nullptr, nullptr, 0, nullptr, nullptr, (double)h->n,
                             dr, scal, partials, ticket, h->stream));
     TRY(gi::launch_center(h->n, npad, dr, nullptr, scal, drt, partials, ticket, h->stream));
-    TRY(gi::launch_aty_fast(h->desc(), static_cast<const uint8_t*>(h->gmiss->ptr), drt, h->du(),
-                            h->dv(), static_cast<const int32_t*>(h->s1cnt->ptr), scal, 1.0,
+    TRY(gi::launch_aty_fast(h->desc(), static_cast<const uint8_t*>(h->gmiss->ptr), drt, du, dv,
+                            static_cast<const int32_t*>(h->s1cnt->ptr), scal, 1.0,
                             h->s_b.as<double>(), h->sms, h->stream));
   }
   GI_CUDA_TRY(cudaMemcpyAsync(out, h->s_b.mem->ptr, sizeof(double) * h->p,
                               cudaMemcpyDeviceToHost, h->stream));
+  return 0;
+}
+
+int gi_aty(gi_matrix* h, const double* r, double sum_r, double* out, int mode) {
+  CHECK_ARG(h && r && out, "NULL argument");
+  if (h->p == 0) return 0;
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard g(h->device);
+  TRY(aty_enqueue(h, r, sum_r, h->du(), h->dv(), out, mode));
+  GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int gi_aty_batched(gi_matrix* h, const double* R, const double* sum_R, const double* U,
+                   const double* V, int64_t B, double* G, int mode) {
+  CHECK_ARG(h && (B == 0 || (R && G)), "NULL argument");
+  CHECK_ARG(B >= 0, "negative batch size");
+  CHECK_ARG((U == nullptr) == (V == nullptr), "U and V must both be given or both be NULL");
+  CHECK_ARG(mode != 0 || B == 0 || sum_R != nullptr, "mode 0 needs the residual sums");
+  if (h->p == 0 || B == 0) return 0;
+  std::lock_guard<std::mutex> lock(h->mu);
+  DeviceGuard g(h->device);
+  const int64_t p = h->p;
+  double *du = h->du(), *dv = h->dv();
+  if (U) {
+    TRY(h->s_d.ensure(sizeof(double) * 2 * p, h->device));
+    du = h->s_d.as<double>();
+    dv = du + p;
+  }
+  for (int64_t b = 0; b < B; ++b) {
+    if (U) {  // stream-ordered: the previous sweep has read the previous stats
+      GI_CUDA_TRY(cudaMemcpyAsync(du, U + b * p, sizeof(double) * p, cudaMemcpyHostToDevice,
+                                  h->stream));
+      GI_CUDA_TRY(cudaMemcpyAsync(dv, V + b * p, sizeof(double) * p, cudaMemcpyHostToDevice,
+                                  h->stream));
+    }
+    TRY(aty_enqueue(h, R + b * h->n, sum_R ? sum_R[b] : 0.0, du, dv, G + b * p, mode));
+  }
   GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }

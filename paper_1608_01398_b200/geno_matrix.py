@@ -284,6 +284,31 @@ class PackedGenotypeMatrix:
                            0 if mode == "exact" else 1))
         return out
 
+    def aty_batched(self, R, U=None, V=None, mode: str = "exact") -> np.ndarray:
+        """aty_genetic for each row of R (B, n) -- e.g. CV fold residuals, zero
+        off the fold -- optionally under per-row stats U, V (B, p); returns
+        (B, p).  Row b equals aty_genetic(R[b]) on with_stats(U[b], V[b]),
+        bit for bit in exact mode.  One device call (gi_aty_batched)."""
+        R = np.ascontiguousarray(np.atleast_2d(R), dtype=np.float64)
+        if R.ndim != 2 or R.shape[1] != self.n:
+            raise ValueError(f"residual matrix must have {self.n} columns")
+        B = R.shape[0]
+        if (U is None) != (V is None):
+            raise ValueError("pass both U and V, or neither")
+        if U is not None:
+            U = np.ascontiguousarray(U, dtype=np.float64)
+            V = np.ascontiguousarray(V, dtype=np.float64)
+            if U.shape != (B, self.p) or V.shape != (B, self.p):
+                raise ValueError("stats matrices must be (batch, variants)")
+        out = np.zeros((B, self.p))
+        if self.p == 0 or self.n == 0 or B == 0:
+            return out
+        sums = np.array([float(r.sum()) for r in R])
+        check(lib().gi_aty_batched(self._h.raw, ptr(R), ptr(sums),
+                                   None if U is None else ptr(U), None if V is None else ptr(V),
+                                   B, ptr(out), 0 if mode == "exact" else 1))
+        return out
+
     def decompress(self, idx) -> np.ndarray:
         """Dense standardized (n, k) submatrix (reference :366-373)."""
         idx = self._check_index(idx)
