@@ -106,6 +106,12 @@ struct FastArgs {
   double* out;
   int64_t n_items;
   unsigned long long* gmax;  // optional: atomicMax of |out_j| (bits of a non-negative double)
+  // optional: the last CTA to finish copies these segments (gradient entries
+  // included, read through L2) into pub_out -- mapped host memory of the
+  // native loop -- so the refresh needs no separate publish launch
+  PubArgs pub;
+  unsigned int* pub_ticket;
+  unsigned long long* pub_out;
 };
 
 __device__ __forceinline__ float dose_term(int code, float r) {
@@ -394,12 +400,31 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
     }
     __syncthreads();  // accumulators, flags and table are reused by the next item
   }
+  if (a.pub_ticket) {
+    // no static shared memory here (the dynamic carve-out is the maximum):
+    // thread 0 takes the ticket, __syncthreads_or broadcasts "last CTA"
+    __threadfence();
+    __syncthreads();
+    int last = 0;
+    if (tid == 0) last = atomicAdd(a.pub_ticket, 1u) == gridDim.x - 1;
+    if (__syncthreads_or(last)) {
+      __threadfence();
+      for (int q = 0; q < a.pub.nseg; ++q) {
+        const PubSeg sg = a.pub.seg[q];
+        const unsigned long long* src = static_cast<const unsigned long long*>(sg.src);
+        for (int64_t e = tid; e < sg.count; e += blockDim.x)
+          a.pub_out[sg.dst + e] = __ldcg(sg.idx ? src + sg.idx[e] : src + e);
+      }
+      if (tid == 0) *a.pub_ticket = 0u;
+    }
+  }
 }
 
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
                     const double* u, const double* v, const int32_t* s1cnt,
                     const double* d_scal, double scale, double* out, int num_sms,
-                    cudaStream_t s, double* d_gmax) {
+                    cudaStream_t s, double* d_gmax, const PubArgs* pub,
+                    unsigned int* pub_ticket, void* pub_out) {
   if (m.p == 0) return 0;
 
   static std::once_flag once;
@@ -420,6 +445,14 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
   a.scale = scale;
   a.out = out;
   a.gmax = reinterpret_cast<unsigned long long*>(d_gmax);
+  if (pub && pub_ticket && pub_out) {
+    a.pub = *pub;
+    a.pub_ticket = pub_ticket;
+    a.pub_out = static_cast<unsigned long long*>(pub_out);
+  } else {
+    a.pub_ticket = nullptr;
+    a.pub_out = nullptr;
+  }
   const int64_t per_wave = (int64_t)num_sms * kMaxGroups;
   int64_t items = (int64_t)num_sms * ((m.G + per_wave - 1) / per_wave);
   if (items > m.G) items = m.G;

@@ -78,6 +78,12 @@ __host__ __device__ inline int64_t byte_offset(int64_t j, int64_t b, int64_t G) 
 int launch_residual(int64_t n, const double* y, const double* fit, const double* C, int c,
                     const double* bcov, const uint8_t* keep, double n_eff, double* r,
                     double* scal, double* partials, unsigned int* ticket, cudaStream_t s);
+// residual + optional beta writes + (gcov != NULL) covariate gradient, fused
+int launch_refresh_residual(int64_t n, const double* y, const double* fit, const double* C,
+                            int c, const double* bcov, const uint8_t* keep, double n_eff,
+                            double* r, double* scal, double* gcov, int64_t sk,
+                            const int64_t* sidx, const double* sval, double* beta,
+                            double* partials, unsigned int* ticket, cudaStream_t s);
 int launch_center(int64_t n, int64_t n_pad, const double* r, const uint8_t* keep, double* scal,
                   float* rt, double* partials, unsigned int* ticket, cudaStream_t s);
 int launch_covgrad(int64_t n, const double* C, int c, const double* r, double* gcov,
@@ -162,7 +168,8 @@ int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
                     const double* u, const double* v, const int32_t* s1cnt,
                     const double* d_scal, double scale, double* out, int num_sms,
-                    cudaStream_t s, double* d_gmax = nullptr);
+                    cudaStream_t s, double* d_gmax = nullptr, const PubArgs* pub = nullptr,
+                    unsigned int* pub_ticket = nullptr, void* pub_out = nullptr);
 int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u,
                      const double* v, const double* d_sum_r, double scale, double* out,
                      cudaStream_t s);

@@ -121,7 +121,7 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   TRY(ws->dalloc(ws->beta, p));
   TRY(ws->dalloc(ws->cvec, 2 * std::max<int64_t>(c, 1)));
   TRY(ws->dalloc(ws->scal, 8));
-  TRY(ws->dalloc(ws->partials, 8 * 296));
+  TRY(ws->dalloc(ws->partials, 16 * 296));
   TRY(ws->dalloc(ws->u, p));
   TRY(ws->dalloc(ws->v, p));
   TRY(ws->dalloc(ws->rt, ws->npad));
@@ -241,46 +241,46 @@ class NativeFit {
     TRY(stage(lw.data(), (int64_t)lw.size(), d_w));
     TRY(stage(bcov.data(), ws_->c, d_cov));
     TRY(flush());
-    if (pend_k_) {
-      TRY(gi::launch_scatter(pend_k_, pend_idx_, pend_w_, ws_->beta, s));
-      ++launches;
-      pend_k_ = 0;
-    }
     if (has_fit) {
       TRY(gi::launch_ax(d, ws_->u, ws_->v, d_sup, d_w, (int64_t)lsup.size(), ws_->fitb, 0, s));
       ++launches;
       // X_S b summed over the shards (NCCL in place on this stream)
       if (sharded()) TRY(comm_->allreduce_device(ws_->fitb, ws_->n, 0, s));
     }
+    // residual + loss + mean, the pending beta writes and g_cov = -C^T r in one
+    // kernel (g_cov in a second one only beyond 8 covariates)
     const uint8_t* keep = masked_ ? ws_->keep : nullptr;
-    TRY(gi::launch_residual(ws_->n, ws_->y, has_fit ? ws_->fitb : nullptr,
-                            ws_->c ? ws_->C : nullptr, (int)ws_->c, d_cov, keep, n_eff_,
-                            ws_->r, ws_->scal, ws_->partials, ws_->ticket, s));
+    TRY(gi::launch_refresh_residual(ws_->n, ws_->y, has_fit ? ws_->fitb : nullptr,
+                                    ws_->c ? ws_->C : nullptr, (int)ws_->c, d_cov, keep, n_eff_,
+                                    ws_->r, ws_->scal, ws_->c ? ws_->cvec + ws_->c : nullptr,
+                                    pend_k_, pend_idx_, pend_w_, ws_->beta, ws_->partials,
+                                    ws_->ticket, s));
+    pend_k_ = 0;
+    launches += ws_->c > 8 ? 1 + (ws_->c + 7) / 8 : 1;
     TRY(gi::launch_center(ws_->n, ws_->npad, ws_->r, keep, ws_->scal, ws_->rt, ws_->partials,
                           ws_->ticket, s));
-    launches += 2;
-    if (ws_->p) {
-      if (ev0) GI_CUDA_TRY(cudaEventRecord(ev0, s));
-      TRY(gi::launch_aty_fast(d, static_cast<const uint8_t*>(h_->gmiss->ptr), ws_->rt, ws_->u,
-                              ws_->v, ws_->s1cnt, ws_->scal, -1.0, ws_->g, h_->sms, s,
-                              ws_->scal + 3));  // max|g| fused into the epilogue
-      if (ev1) GI_CUDA_TRY(cudaEventRecord(ev1, s));
-      ++aty_launches;
-      ++launches;
-    }
-    if (ws_->c) {
-      TRY(gi::launch_covgrad(ws_->n, ws_->C, (int)ws_->c, ws_->r, ws_->cvec + ws_->c,
-                             ws_->partials, ws_->ticket, s));
-      ++launches;
-    }
-    // scal, g_cov and g on the (local) support -> mapped host memory, one launch
+    ++launches;
+    // scal, g_cov and g on the (local) support -> mapped host memory, written by
+    // the last CTA of the X^T r kernel (a separate launch only when p == 0)
     const int64_t ks = (int64_t)lsup.size();
     gi::PubArgs pub;
     pub.add(ws_->scal, 8, ws_->oR);
     pub.add(ws_->cvec + ws_->c, ws_->c, ws_->oR + 8);
     pub.add(ws_->g, ks, ws_->oR + 8 + ws_->c, d_sup);
-    TRY(gi::launch_publish(pub, ws_->dmap, s));
-    ++launches;
+    if (ws_->p) {
+      if (ev0) GI_CUDA_TRY(cudaEventRecord(ev0, s));
+      TRY(gi::launch_aty_fast(d, static_cast<const uint8_t*>(h_->gmiss->ptr), ws_->rt, ws_->u,
+                              ws_->v, ws_->s1cnt, ws_->scal, -1.0, ws_->g, h_->sms, s,
+                              ws_->scal + 3,  // max|g| fused into the epilogue
+                              &pub, ws_->ticket, ws_->dmap));
+      if (ev1) GI_CUDA_TRY(cudaEventRecord(ev1, s));
+      ++aty_launches;
+      ++launches;
+    }
+    if (!ws_->p) {
+      TRY(gi::launch_publish(pub, ws_->dmap, s));
+      ++launches;
+    }
     TRY(sync());
     const double* ho = ws_->hmap + ws_->oR;
     if (ev0 && ws_->p) {

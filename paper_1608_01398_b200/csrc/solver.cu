@@ -124,6 +124,69 @@ __global__ void residual_kernel(int64_t n, const double* __restrict__ y,
     }
   }
 }
+// Refresh prologue of the native loop: optional beta writes (block 0:
+// beta[sidx[t]] = sval[t]), the residual as residual_kernel, and with kCov the
+// covariate gradient gcov[l] = -sum_i C[i, l] r_i of covgrad_kernel in the
+// same pass -- same grid, per-thread order and block-order fold, so the same
+// bits as the two separate kernels.  Partials: 10 per block.
+template <bool kCov>
+__global__ void refresh_residual_kernel(int64_t n, const double* __restrict__ y,
+                                        const double* __restrict__ fit,
+                                        const double* __restrict__ C, int c,
+                                        const double* __restrict__ bcov,
+                                        const uint8_t* __restrict__ keep, double n_eff,
+                                        double* __restrict__ r, double* __restrict__ scal,
+                                        double* __restrict__ gcov, int64_t sk,
+                                        const int64_t* __restrict__ sidx,
+                                        const double* __restrict__ sval,
+                                        double* __restrict__ beta, RedWs ws) {
+  constexpr int NV = kCov ? 10 : 2;
+  __shared__ double sh[NV * 32];
+  if (blockIdx.x == 0)
+    for (int64_t t = threadIdx.x; t < sk; t += blockDim.x) beta[sidx[t]] = sval[t];
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double ri = 0.0;
+    if (!keep || keep[i]) {
+      double f = fit ? fit[i] : 0.0;
+      if (c > 0) {
+        double cb = 0.0;
+        for (int l = 0; l < c; ++l) cb = __dadd_rn(cb, __dmul_rn(C[i * c + l], bcov[l]));
+        f = fit ? __dadd_rn(f, cb) : cb;
+      }
+      ri = __dsub_rn(y[i], f);
+    }
+    r[i] = ri;
+    acc[0] += ri * ri;
+    acc[1] += ri;
+    if (kCov) {
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (l < c) acc[2 + l] += C[i * c + l] * ri;
+    }
+  }
+  block_sum<NV>(acc, sh);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < NV; ++q) ws.partials[blockIdx.x * NV + q] = acc[q];
+  if (last_block(ws.ticket) && threadIdx.x < 32) {
+    const double s2 = fold_sum(ws.partials, NV, 0, gridDim.x);
+    const double s1 = fold_sum(ws.partials, NV, 1, gridDim.x);
+    double gl[8];
+    if (kCov)
+      for (int l = 0; l < c; ++l) gl[l] = fold_sum(ws.partials, NV, 2 + l, gridDim.x);
+    if (threadIdx.x == 0) {
+      scal[0] = 0.5 * s2;
+      scal[1] = n_eff > 0.0 ? s1 / n_eff : 0.0;
+      if (kCov)
+        for (int l = 0; l < c; ++l) gcov[l] = -gl[l];
+      *ws.ticket = 0u;
+    }
+  }
+}
+
 
 // rt_i = keep_i ? fp32(r_i - mean) : 0 over the padded length; scal[2] = sum rt.
 __global__ void center_kernel(int64_t n, int64_t n_pad, const double* __restrict__ r,
@@ -293,6 +356,23 @@ static int red_grid(int64_t m) {
   if (g > kRedBlocks) g = kRedBlocks;
   if (g < 1) g = 1;
   return (int)g;
+}
+
+int launch_refresh_residual(int64_t n, const double* y, const double* fit, const double* C,
+                            int c, const double* bcov, const uint8_t* keep, double n_eff,
+                            double* r, double* scal, double* gcov, int64_t sk,
+                            const int64_t* sidx, const double* sval, double* beta,
+                            double* partials, unsigned int* ticket, cudaStream_t s) {
+  RedWs ws{partials, ticket};
+  if (gcov && c > 0 && c <= 8)
+    refresh_residual_kernel<true><<<red_grid(n), kRedThreads, 0, s>>>(
+        n, y, fit, C, c, bcov, keep, n_eff, r, scal, gcov, sk, sidx, sval, beta, ws);
+  else
+    refresh_residual_kernel<false><<<red_grid(n), kRedThreads, 0, s>>>(
+        n, y, fit, C, c, bcov, keep, n_eff, r, scal, nullptr, sk, sidx, sval, beta, ws);
+  GI_LAUNCH_CHECK();
+  if (gcov && c > 8) return launch_covgrad(n, C, c, r, gcov, partials, ticket, s);
+  return 0;
 }
 
 int launch_residual(int64_t n, const double* y, const double* fit, const double* C, int c,
