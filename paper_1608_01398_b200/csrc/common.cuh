@@ -120,8 +120,6 @@ int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double
                 int64_t* out_idx, double* out_val, uint64_t* out_key, int64_t* out_count,
                 cudaStream_t s, const double* mu_dev = nullptr,
                 unsigned int* ticket = nullptr);
-int launch_ratio(double num, double* scal, int den, int out, cudaStream_t s);
-int launch_mask(int64_t n, const uint8_t* keep, double* x, cudaStream_t s);
 int launch_scatter(int64_t k, const int64_t* idx, const double* val, double* beta,
                    cudaStream_t s);
 int launch_gather(int64_t k, const int64_t* idx, const double* src, double* dst,

@@ -726,31 +726,6 @@ int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double
   return 0;
 }
 
-// scal[out] = num / scal[den]  (the normalised step on the device, iht.py:244)
-__global__ void ratio_kernel(double num, double* scal, int den, int out) {
-  scal[out] = num / scal[den];
-}
-
-int launch_ratio(double num, double* scal, int den, int out, cudaStream_t s) {
-  ratio_kernel<<<1, 1, 0, s>>>(num, scal, den, out);
-  GI_LAUNCH_CHECK();
-  return 0;
-}
-
-// x[i] = keep[i] ? x[i] : 0
-__global__ void mask_kernel(int64_t n, const uint8_t* __restrict__ keep, double* __restrict__ x) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    if (!keep[i]) x[i] = 0.0;
-}
-
-int launch_mask(int64_t n, const uint8_t* keep, double* x, cudaStream_t s) {
-  if (n <= 0) return 0;
-  mask_kernel<<<red_grid(n), kRedThreads, 0, s>>>(n, keep, x);
-  GI_LAUNCH_CHECK();
-  return 0;
-}
-
 // dense beta update: beta[idx[t]] = val[t]
 __global__ void scatter_kernel(int64_t k, const int64_t* __restrict__ idx,
                                const double* __restrict__ val, double* __restrict__ beta) {
