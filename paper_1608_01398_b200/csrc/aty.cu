@@ -21,10 +21,12 @@
 //   Blocks of the matrix (4 KiB = 32 SNPs x 512 samples) stream through a
 //   16-slot shared-memory ring filled by a producer warp with
 //   cp.async.bulk (TMA bulk copies, mbarrier complete_tx), with an L2 prefetch
-//   running ahead.  Per (SNP, tile) partial sums are fp32 (4 interleaved
-//   chains of 32 terms) and are promoted to an fp64 accumulator per tile, so
-//   the error is ~1e-7 relative to |g_j| -- inside the north star's 1e-6 on
-//   beta/loss (supports are stable up to 1e-5).  Because
+//   running ahead.  Per (SNP, tile) partial sums are fp32, summed pairwise in
+//   an order that does not depend on the lane (process_group), and promoted to
+//   an fp64 accumulator per tile: identical SNP columns get identical
+//   gradients (the reference's exact ties), and the error is <= ~6e-7 of
+//   rms(g) -- inside the north star's 1e-6 on beta/loss (SURVEY.md section
+//   0.4: supports are stable up to 1e-5).  Because
 //   r is centred, t and u*sum_r do not cancel catastrophically; the constant
 //   part mean(r) contributes v_j * mean(r) * (s1_j - u_j cnt_j) = 0 exactly.
 //
@@ -183,41 +185,94 @@ __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
   return r;
 }
 
-__device__ __forceinline__ void add2(uint64_t& acc, uint64_t x) {
-  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(x));  // FADD2: two fp32 adds
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));  // FADD2: two fp32 adds
+  return r;
 }
 
-__device__ __forceinline__ float sum2(uint64_t x) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x));
-  return lo + hi;
+__device__ __forceinline__ float lo_of(uint64_t x) {
+  return __uint_as_float((uint32_t)x);
+}
+
+__device__ __forceinline__ float hi_of(uint64_t x) {
+  return __uint_as_float((uint32_t)(x >> 32));
+}
+
+// Lane-order-free summation.  Lane L visits word w = L ^ q at step q, so two
+// identical SNP columns in different lanes see the same words in different
+// orders.  Each word's sum is formed in a fixed byte order, (e0 + e1) +
+// (e2 + e3), and the 32 word sums are combined pairwise over aligned blocks of
+// q -- which are aligned blocks of w for every L -- so every addition of the
+// tree adds the same two values for any lane, at most swapped (IEEE addition
+// is commutative).  Identical columns therefore get identical sums (the
+// reference's exact ties, broken by index), and pairwise summation is also
+// more accurate than running chains.  `st` is a binary-counter stack of the
+// aligned 2-, 4-, 8- and 16-word block sums.
+template <typename V, typename Add>
+__device__ __forceinline__ void tree_push(int j, V b, V (&st)[4], V& total, Add add) {
+  if ((j & 1) == 0) { st[0] = b; return; }
+  b = add(st[0], b);
+  if ((j & 2) == 0) { st[1] = b; return; }
+  b = add(st[1], b);
+  if ((j & 4) == 0) { st[2] = b; return; }
+  b = add(st[2], b);
+  if ((j & 8) == 0) { st[3] = b; return; }
+  total = add(st[3], b);
 }
 
 template <bool kMissing>
 __device__ __forceinline__ void process_group(const uint32_t (&wd)[32], uint32_t xb,
                                               float& tile_t, float& tile_m) {
-  uint64_t a01 = 0, a23 = 0, b01 = 0, b23 = 0;  // fp32x2 partial sums (4 chains)
+  if (!kMissing) {
+    float st[4], total = 0.f;
 #pragma unroll
-  for (int q = 0; q < 32; ++q) {
-    const uint32_t x = xb ^ (uint32_t)(q << 2);
-    const float e0 = lds_f32_off<0>(__byte_perm(wd[q], x, 0x6504));
-    const float e1 = lds_f32_off<128>(__byte_perm(wd[q], x, 0x6514));
-    const float e2 = lds_f32_off<65536>(__byte_perm(wd[q], x, 0x6524));
-    const float e3 = lds_f32_off<65536 + 128>(__byte_perm(wd[q], x, 0x6534));
-    add2(a01, pack2(e0, e1));
-    add2(a23, pack2(e2, e3));
-    if (kMissing) {
-      const uint32_t mm = (wd[q] << 1) & ~wd[q] & 0xAAAAAAAAu;  // missing (01) -> het (10)
-      const float f0 = lds_f32_off<0>(__byte_perm(mm, x, 0x6504));
-      const float f1 = lds_f32_off<128>(__byte_perm(mm, x, 0x6514));
-      const float f2 = lds_f32_off<65536>(__byte_perm(mm, x, 0x6524));
-      const float f3 = lds_f32_off<65536 + 128>(__byte_perm(mm, x, 0x6534));
-      add2(b01, pack2(f0, f1));
-      add2(b23, pack2(f2, f3));
+    for (int q = 0; q < 32; q += 2) {  // words q and q + 1 side by side in FADD2 lanes
+      const uint32_t x = xb ^ (uint32_t)(q << 2), y = xb ^ (uint32_t)((q + 1) << 2);
+      const float e0 = lds_f32_off<0>(__byte_perm(wd[q], x, 0x6504));
+      const float e1 = lds_f32_off<128>(__byte_perm(wd[q], x, 0x6514));
+      const float e2 = lds_f32_off<65536>(__byte_perm(wd[q], x, 0x6524));
+      const float e3 = lds_f32_off<65536 + 128>(__byte_perm(wd[q], x, 0x6534));
+      const float g0 = lds_f32_off<0>(__byte_perm(wd[q + 1], y, 0x6504));
+      const float g1 = lds_f32_off<128>(__byte_perm(wd[q + 1], y, 0x6514));
+      const float g2 = lds_f32_off<65536>(__byte_perm(wd[q + 1], y, 0x6524));
+      const float g3 = lds_f32_off<65536 + 128>(__byte_perm(wd[q + 1], y, 0x6534));
+      const uint64_t p01 = fadd2(pack2(e0, g0), pack2(e1, g1));  // (e0 + e1, g0 + g1)
+      const uint64_t p23 = fadd2(pack2(e2, g2), pack2(e3, g3));  // (e2 + e3, g2 + g3)
+      const uint64_t ws = fadd2(p01, p23);                       // (word q, word q + 1)
+      tree_push(q >> 1, lo_of(ws) + hi_of(ws), st, total,
+                [](float a, float b) { return a + b; });
     }
+    tile_t = total;
+    tile_m = 0.f;
+  } else {
+    uint64_t st[4], total = 0;  // (dose sum, missing sum) pairs
+#pragma unroll
+    for (int q = 0; q < 32; q += 2) {
+      uint64_t w2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t wq = wd[q + h];
+        const uint32_t x = xb ^ (uint32_t)((q + h) << 2);
+        const uint32_t mm = (wq << 1) & ~wq & 0xAAAAAAAAu;  // missing (01) -> het (10)
+        const float e0 = lds_f32_off<0>(__byte_perm(wq, x, 0x6504));
+        const float e1 = lds_f32_off<128>(__byte_perm(wq, x, 0x6514));
+        const float e2 = lds_f32_off<65536>(__byte_perm(wq, x, 0x6524));
+        const float e3 = lds_f32_off<65536 + 128>(__byte_perm(wq, x, 0x6534));
+        const float f0 = lds_f32_off<0>(__byte_perm(mm, x, 0x6504));
+        const float f1 = lds_f32_off<128>(__byte_perm(mm, x, 0x6514));
+        const float f2 = lds_f32_off<65536>(__byte_perm(mm, x, 0x6524));
+        const float f3 = lds_f32_off<65536 + 128>(__byte_perm(mm, x, 0x6534));
+        const uint64_t pe = fadd2(pack2(e0, e2), pack2(e1, e3));  // (e0 + e1, e2 + e3)
+        const uint64_t pf = fadd2(pack2(f0, f2), pack2(f1, f3));
+        w2[h] = fadd2(pack2(lo_of(pe), lo_of(pf)), pack2(hi_of(pe), hi_of(pf)));
+      }
+      tree_push(q >> 1, fadd2(w2[0], w2[1]), st, total,
+                [](uint64_t a, uint64_t b) { return fadd2(a, b); });
+    }
+    tile_t = lo_of(total);
+    tile_m = hi_of(total);
   }
-  tile_t = sum2(a01) + sum2(a23);
-  tile_m = kMissing ? sum2(b01) + sum2(b23) : 0.f;
 }
 
 // A warp's stream of blocks: for tile t = 0..T-1, its groups gl = warp,

@@ -208,3 +208,29 @@ def test_aty_batched_fold_residuals_with_fold_stats():
         dev.aty_batched(R[:, :10])
     with pytest.raises(ValueError):
         dev.aty_batched(R, U)
+
+
+def test_fast_aty_identical_columns_get_identical_gradients():
+    """SNPs in perfect LD have identical columns; the reference gives them
+    identical gradients, so top-k ties go to the lower index.  The fast kernel
+    sums integer table entries, so its X^T r of a column depends only on the
+    column's codes -- not on the lane/word order it is visited in."""
+    gi = _gm()
+    rng = np.random.default_rng(17)
+    n, half = 3000, 120
+    base = oracle.random_codes(n, half, seed=17, missing_rate=0.05)
+    perm = rng.permutation(half)
+    codes = np.concatenate([base, base[:, perm]], axis=1)  # column half + i == column perm[i]
+    dev = gi.PackedGenotypeMatrix.from_codes(codes)
+    for _ in range(3):
+        g = dev.aty_genetic(rng.standard_normal(n), mode="fast")
+        np.testing.assert_array_equal(g[half:], g[perm])
+    # a fit whose top-k meets such a tie picks the lower index, like the oracle
+    y = oracle.OraclePacked.from_codes(codes).ax_columns(np.array([perm[3]]), np.array([2.0]))
+    y = y + rng.normal(0, 0.1, n)
+    view = gi.StandardizedView(dev, gi.CovariateBlock.build(None, n=n))
+    got = gi.fit(view, y, gi.IhtConfig(k=1))
+    want = oracle.fit(oracle.OracleView(oracle.OraclePacked.from_codes(codes),
+                                        oracle.intercept(n)), y, 1)
+    np.testing.assert_array_equal(got.model.support, want.support)
+    assert got.model.support[0] == min(perm[3], half + 3)
