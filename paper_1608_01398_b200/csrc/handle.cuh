@@ -43,9 +43,12 @@ struct DevMem {
   }
 };
 
-// The device's default stream-ordered pool, set to keep freed memory mapped:
-// CV fold copies and fit workspaces are allocated and dropped repeatedly, and
-// re-mapping gigabytes through cudaMalloc/cudaFree costs milliseconds each.
+// The device's default stream-ordered pool, set to keep up to a quarter of the
+// device memory mapped after frees: CV fold copies and fit workspaces are
+// allocated and dropped repeatedly, and re-mapping gigabytes through
+// cudaMalloc/cudaFree costs milliseconds each.  Beyond that the driver returns
+// freed memory at synchronisation points, so other allocators (torch) and
+// processes get it back.
 inline cudaMemPool_t device_pool(int device) {
   static std::mutex mu;
   static bool configured[64] = {};
@@ -53,7 +56,13 @@ inline cudaMemPool_t device_pool(int device) {
   if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
   if (device >= 0 && device < 64 && !configured[device]) {
-    uint64_t keep = UINT64_MAX;
+    size_t free_b = 0, total_b = 0;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaMemGetInfo(&free_b, &total_b);
+    cudaSetDevice(prev);
+    uint64_t keep = (uint64_t)total_b / 4;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     configured[device] = true;
   }
