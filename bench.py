@@ -65,15 +65,20 @@ def parse():
     ap.add_argument("--cpu-slice", type=int, default=0,
                     help="SNPs in the CPU-baseline sample (0 = auto, ~2.5 GB)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2path", "c4cv"],
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2path", "c4cv", "c5"],
                     help="c3 (default, the metric's config), c2path (BASELINE config 2: "
                          "k=10..50 model-size path at n=5k x p=100k), c4cv (config 4: "
-                         "5-fold CV over k=1..20 at n=20k x p=500k)")
-    return ap.parse_args()
+                         "5-fold CV over k=1..20 at n=20k x p=500k), c5 (config 5: "
+                         "n=p=500k, 2%% missing, k=100; 62.5 GB)")
+    a = ap.parse_args()
+    if a.workload == "c5":  # same measurement as c3 on the UK-Biobank-scale shape
+        a.n, a.p, a.k, a.missing = 500_000, 500_000, 100, 0.02
+    return a
 
 
 def config_of(a, world):
-    return {"workload": f"BASELINE config 3: synthetic BED n={a.n} x p={a.p} "
+    which = "5" if a.workload == "c5" else "3"
+    return {"workload": f"BASELINE config {which}: synthetic BED n={a.n} x p={a.p} "
                         f"({a.p * ((a.n + 3) // 4) / 1e9:.1f} GB packed), k={a.k}, "
                         f"k_true={a.k}, intercept covariate, missing={a.missing}",
             "n": a.n, "p": a.p, "k": a.k, "step": "one cold-start IHT fit to convergence",
@@ -90,7 +95,7 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def smem_roofline(n, p, ms, sm_mhz, sms, missing):
+def smem_roofline(n, p, ms, sm_mhz, sms, missing, miss_group_frac=None):
     """Secondary roofline of aty_fast_kernel: its shared-memory traffic against
     the SM crossbar (128 B/clk/SM, B300_MICROARCH.md "LDS/STS") at the SM clock
     sampled during the run.  LSU shared-memory traffic per byte of the tiled
@@ -100,20 +105,24 @@ def smem_roofline(n, p, ms, sm_mhz, sms, missing):
     copy path, not the LSU crossbar: this count matches ncu's
     shared-memory LSU wavefronts of the kernel (1.04e9 modelled vs 1.078e9
     measured at config 3, profiles/r01_summary.md).  Groups with a missing
-    genotype add a second 4 B lookup per byte (not counted here)."""
+    genotype add a second 4 B lookup per byte: counted when the fraction of
+    such groups is known (`miss_group_frac`)."""
     if not ms or not sm_mhz:
         return None
     T = (n + 511) // 512
     G = (p + 31) // 32
     per_wave = sms * 112  # kMaxGroups groups per work item (aty.cu)
     items = min(sms * ((G + per_wave - 1) // per_wave), G)
-    smem_bytes = 5 * G * T * 4096 + items * T * 131072
+    per_byte = 5.0 + 4.0 * (miss_group_frac or 0.0)
+    smem_bytes = int(per_byte * G * T * 4096) + items * T * 131072
     achieved = smem_bytes / (ms / 1e3) / 1e9
     peak = 128 * sms * sm_mhz * 1e6 / 1e9
     return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "bytes_per_launch": smem_bytes,
             "peak_basis": f"128 B/clk/SM x {sms} SMs x {sm_mhz:.0f} MHz (median sampled SM clock)",
-            "note": "lower bound when groups carry missing genotypes" if missing else None}
+            "missing_group_fraction": miss_group_frac,
+            "note": ("lower bound: groups with missing genotypes not counted"
+                     if missing and miss_group_frac is None else None)}
 
 
 def traffic_from_profile(n, p):
@@ -353,7 +362,7 @@ def main():
     if a.impl == "reference":
         reference_arm(a)
         return
-    if a.workload != "c3":
+    if a.workload not in ("c3", "c5"):
         secondary(a)
         return
     import torch
@@ -460,6 +469,14 @@ def main():
         return
 
     clk = clocks.summary()
+    # groups of 32 SNPs holding a missing genotype take the second lookup
+    miss_frac = 0.0
+    if a.missing > 0:
+        local_m = geno.local if sharded else geno
+        mc = local_m.missing_counts
+        pad = (-mc.size) % 32
+        miss_frac = float(np.mean(np.concatenate([mc, np.zeros(pad, mc.dtype)])
+                                  .reshape(-1, 32).sum(axis=1) > 0)) if mc.size else 0.0
     # ---- roofline of the X^T r kernel
     n, p_local = a.n, (geno.local.p if sharded else a.p)
     nb = (n + 3) // 4
@@ -497,7 +514,8 @@ def main():
                      "kernel": "aty_fast_kernel", "bytes_per_launch": alg_bytes,
                      "smem": smem_roofline(n, p_local, aty_avg, clk.get("sm_mhz"),
                                            torch.cuda.get_device_properties(local)
-                                           .multi_processor_count, a.missing)},
+                                           .multi_processor_count, a.missing,
+                                           miss_frac)},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h // max(a.steps, 1)},
