@@ -218,9 +218,80 @@ def auto_slice(n):
     return max(1000, int(2.5e9 // nb))
 
 
+def secondary_shape(workload):
+    """(n, p, k_true, path) of the config-2 / config-4 workloads."""
+    if workload == "c2path":
+        return 5000, 100_000, 20, np.arange(10, 51)
+    return 20_000, 500_000, 10, np.arange(1, 21)
+
+
+def reference_secondary(a):
+    """Reference arm of --workload c2path / c4cv, on the host only: the same
+    bytes (CPU twin of the device generator) and the same phenotype draws
+    (simulate.py's rng sequence, X_S b through the oracle's bit-exact ax)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    n, p, k_true, path = secondary_shape(a.workload)
+    threads = os.cpu_count() or 1
+    oracle.set_threads(threads)
+    ref = oracle.OraclePacked.from_bed(oracle.synth_bed(a.seed, n, 0, p, missing=a.missing), n)
+    rng = np.random.default_rng(a.pheno_seed)  # simulate_phenotype (simulate.py:68-83)
+    causal = np.sort(rng.choice(p, size=k_true, replace=False)).astype(np.int64)
+    effects = rng.normal(0.0, np.sqrt(0.01), size=k_true)
+    y = ref.ax_columns(causal, effects) + rng.normal(0.0, np.sqrt(0.01), size=n)
+    view = oracle.OracleView(ref, oracle.intercept(n))
+    line = {"impl": "reference", "metric": METRIC, "unit": "it/s", "n_gpus": a.gpus,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "steps": a.steps, "warmup": a.warmup}
+    if a.workload == "c2path":
+        line["config"] = {"workload": f"BASELINE config 2: n={n} x p={p}, model-size path "
+                                      f"k=10..50 (41 cold fits), k_true={k_true}",
+                          "step": "all 41 fits of the path"}
+        times, iters = [], 0
+        for step in range(a.warmup + a.steps):
+            t0 = time.perf_counter()
+            fits = [oracle.fit(view, y, int(k)) for k in path]
+            if step >= a.warmup:
+                times.append(time.perf_counter() - t0)
+                iters = sum(f.iterations for f in fits)
+        t = statistics.median(times)
+        line.update(value=iters / t, ms_per_step=1e3 * t,
+                    cpu_baseline={"value": iters / t, "unit": "it/s", "cores": threads,
+                                  "kind": "port", "sample": "the full 41-fit path on the oracle"})
+    else:
+        line["config"] = {"workload": f"BASELINE config 4: n={n} x p={p}, 5-fold CV over "
+                                      f"k=1..20 + final fit and refit, k_true={k_true}, "
+                                      f"fold seed 2016", "step": "one cv_iht call"}
+        labels = oracle.folds(n, 5, 2016)
+        train, test = np.flatnonzero(labels != 0), np.flatnonzero(labels == 0)
+        t0 = time.perf_counter()
+        g_train = ref.subset_rows(train)
+        ref.subset_rows(test)
+        t_repack = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        fold_fit = oracle.fit(oracle.OracleView(g_train, oracle.intercept(train.size)),
+                              y[train], k_true)
+        t_fit = time.perf_counter() - t0
+        t_cv = 5 * t_repack + 101 * t_fit
+        line.update(value=None, cv_seconds=t_cv, ms_per_step=1e3 * t_cv,
+                    cpu_baseline={"value": 1.0 / t_cv, "unit": "cv/s", "cores": threads,
+                                  "kind": "port",
+                                  "sample": f"one fold re-pack ({t_repack:.1f} s, x5) + one fit "
+                                            f"at k={k_true} ({fold_fit.iterations} iterations, "
+                                            f"{t_fit:.2f} s, x101 fits), extrapolated"})
+    v = line["value"] if line["value"] is not None else 1.0 / line["cv_seconds"]
+    line["e2e"] = {"value": v, "unit": line["unit"] if line["value"] is not None else "cv/s",
+                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    print(json.dumps(line), flush=True)
+
+
 def reference_arm(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return
+    if a.workload in ("c2path", "c4cv"):
+        reference_secondary(a)
         return
     p_slice = min(a.p, a.cpu_slice or auto_slice(a.n))
     times, threads = cpu_slice_sweep(a.n, p_slice, a.seed, a.missing, a.warmup + a.steps)
@@ -235,7 +306,8 @@ def reference_arm(a):
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": 1e3 * t_iter, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_of(a, 1),
+            "config": config_of(a, a.gpus),  # the workload our arm runs at this N
+            "host": "reference algorithm on the box's host cores (no GPU)",
             "xtr_packed_gbs": p_slice * nb / statistics.median(timed) / 1e9,
             "cpu_baseline": {"value": value, "unit": "it/s", "cores": threads, "kind": "port",
                              "sample": sample},
@@ -262,10 +334,7 @@ def secondary(a):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
 
-    if a.workload == "c2path":
-        n, p, k_true, path = 5000, 100_000, 20, np.arange(10, 51)
-    else:
-        n, p, k_true, path = 20_000, 500_000, 10, np.arange(1, 21)
+    n, p, k_true, path = secondary_shape(a.workload)
     m = gi.PackedGenotypeMatrix.synthetic(n, p, a.seed, missing_rate=a.missing)
     view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=n))
     y, _ = simulate_phenotype(view, SimulationSpec(k_true=k_true, seed=a.pheno_seed))
