@@ -117,6 +117,33 @@ int gi_comm::allgather_host(const double* send, int64_t count, double* recv, cud
   return 0;
 }
 
+int gi_comm::allgather_device(const double* dsend, int64_t count, double* drecv,
+                              cudaStream_t s) {
+  if (count <= 0) return 0;
+  if (kind == kNccl) {  // also at world 1: a real (local) NCCL collective
+    NCCL_TRY(nccl().all_gather(dsend, drecv, (size_t)count, ncclFloat64,
+                               static_cast<ncclComm_t>(nccl_comm), s));
+    return 0;
+  }
+  if (world <= 1) {
+    GI_CUDA_TRY(cudaMemcpyAsync(drecv, dsend, sizeof(double) * count, cudaMemcpyDeviceToDevice,
+                                s));
+    return 0;
+  }
+  std::vector<double> mine((size_t)count), all((size_t)(count * world));
+  GI_CUDA_TRY(cudaMemcpyAsync(mine.data(), dsend, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                              s));
+  GI_CUDA_TRY(cudaStreamSynchronize(s));
+  if (allgather(ctx, mine.data(), count, all.data()) != 0) {
+    gi_set_error("host all-gather callback failed");
+    return -1;
+  }
+  GI_CUDA_TRY(cudaMemcpyAsync(drecv, all.data(), sizeof(double) * count * world,
+                              cudaMemcpyHostToDevice, s));
+  GI_CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
+
 gi_comm::~gi_comm() {
   if (scratch) cudaFree(scratch);
   if (kind == kNccl && nccl_comm && nccl().ready)

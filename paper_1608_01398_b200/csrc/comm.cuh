@@ -21,5 +21,8 @@ struct gi_comm {
   int allreduce_device(double* dbuf, int64_t count, int op, cudaStream_t s);
   // all-gather of host buffers: recv = world x count, rank-major
   int allgather_host(const double* send, int64_t count, double* recv, cudaStream_t s);
+  // all-gather of device buffers on stream s (NCCL: in the stream, no host
+  // sync; callbacks: staged through the host)
+  int allgather_device(const double* dsend, int64_t count, double* drecv, cudaStream_t s);
   ~gi_comm();
 };

@@ -120,6 +120,14 @@ int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double
                 int64_t* out_idx, double* out_val, uint64_t* out_key, int64_t* out_count,
                 cudaStream_t s, const double* mu_dev = nullptr,
                 unsigned int* ticket = nullptr);
+// sharded loop exchanges (solver.cu): gather this shard's (max|g|, g on the
+// global support), fold the all-gathered rows, merge all-gathered top-k lists
+int launch_shard_gather(int64_t kg, const int64_t* gsel, const double* g, const double* scal3,
+                        double* mine, cudaStream_t s);
+int launch_shard_fold(int world, int64_t kg, const double* all, double* out, cudaStream_t s);
+int launch_shard_merge(int world, int64_t ke, const double* all, uint64_t* ckey, int64_t* cidx,
+                       double* cval, int64_t* out_idx, double* out_val, uint64_t* out_key,
+                       int64_t* out_count, cudaStream_t s);
 int launch_scatter(int64_t k, const int64_t* idx, const double* val, double* beta,
                    cudaStream_t s);
 int launch_gather(int64_t k, const int64_t* idx, const double* src, double* dst,

@@ -54,7 +54,10 @@ struct FitWs {
   // results: mapped pinned host memory written by kernels (device alias dmap)
   double* hmap = nullptr;
   double* dmap = nullptr;
-  int64_t oR = 0, oT = 0, oM = 0, oS = 0;  // regions: refresh, top-k, den/mu, image
+  int64_t oR = 0, oT = 0, oM = 0, oS = 0, oG = 0;  // refresh, top-k, den/mu, image, shards
+  // sharded loop: exchange buffers on the device (grown on demand)
+  double* shard_buf = nullptr;
+  int64_t shard_cap = 0;
   std::vector<void*> dev_allocs;
   bool primed = false, masked = false;
   uint64_t primed_uid = 0;  // handle whose inputs are resident (y == NULL calls)
@@ -65,6 +68,7 @@ struct FitWs {
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     for (void* ptr : dev_allocs) cudaFreeAsync(ptr, stream);
+    if (shard_buf) cudaFreeAsync(shard_buf, stream);
     if (stream) cudaStreamSynchronize(stream);
     if (hin) cudaFreeHost(hin);
     if (hmap) cudaFreeHost(hmap);
@@ -142,7 +146,8 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   ws->oT = 8 + c + kcap;               // count | idx (kcap) | val (kcap) | key (kcap)
   ws->oM = ws->oT + 1 + 3 * kcap;      // den, mu
   ws->oS = ws->oM + 2;                 // ||X d||^2 of a backtracking check
-  GI_CUDA_TRY(cudaHostAlloc(&ws->hmap, sizeof(double) * (size_t)(ws->oS + 2),
+  ws->oG = ws->oS + 2;                 // sharded: global max|g| | g on the support (kcap)
+  GI_CUDA_TRY(cudaHostAlloc(&ws->hmap, sizeof(double) * (size_t)(ws->oG + 1 + kcap),
                             cudaHostAllocMapped));
   GI_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ws->dmap), ws->hmap, 0));
   out = ws;
@@ -240,6 +245,15 @@ class NativeFit {
     TRY(stage(lsup.data(), (int64_t)lsup.size(), d_sup));
     TRY(stage(lw.data(), (int64_t)lw.size(), d_w));
     TRY(stage(bcov.data(), ws_->c, d_cov));
+    // sharded: where each global support entry lives on this shard (or -1)
+    const int64_t kg = (int64_t)sup.size();
+    const int64_t* d_gsel = nullptr;
+    if (sharded()) {
+      std::vector<int64_t> gsel((size_t)kg, -1);
+      for (int64_t t = 0; t < kg; ++t)
+        if (sup[t] >= j_base_ && sup[t] < j_base_ + ws_->p) gsel[t] = sup[t] - j_base_;
+      TRY(stage(gsel.data(), kg, d_gsel));
+    }
     TRY(flush());
     if (has_fit) {
       TRY(gi::launch_ax(d, ws_->u, ws_->v, d_sup, d_w, (int64_t)lsup.size(), ws_->fitb, 0, s));
@@ -281,6 +295,18 @@ class NativeFit {
       TRY(gi::launch_publish(pub, ws_->dmap, s));
       ++launches;
     }
+    if (sharded()) {
+      // one all-gather of (max|g|, this shard's g on the global support, 0
+      // elsewhere), folded in rank order on the device -- no host round trip
+      const int world = comm_->world;
+      TRY(ensure_shard_buf(world));
+      double* mine = ws_->shard_buf;
+      double* allm = mine + (1 + ws_->kcap);
+      TRY(gi::launch_shard_gather(kg, d_gsel, ws_->g, ws_->scal + 3, mine, s));
+      TRY(comm_->allgather_device(mine, 1 + kg, allm, s));
+      TRY(gi::launch_shard_fold(world, kg, allm, ws_->dmap + ws_->oG, s));
+      launches += 2;
+    }
     TRY(sync());
     const double* ho = ws_->hmap + ws_->oR;
     if (ev0 && ws_->p) {
@@ -295,21 +321,24 @@ class NativeFit {
       gsup.assign(ho + 8 + ws_->c, ho + 8 + ws_->c + ks);
       return 0;
     }
-    // one all-gather carries max|g| and the support's gradient entries; each
-    // entry lives on exactly one shard, so summing the zero-padded rows is exact
-    const int64_t kg = (int64_t)sup.size();
-    std::vector<double> mine((size_t)(1 + kg), 0.0), all((size_t)((1 + kg) * comm_->world));
-    mine[0] = gmax;
-    for (int64_t t = 0, l = 0; t < kg; ++t)
-      if (sup[t] >= j_base_ && sup[t] < j_base_ + ws_->p) mine[1 + t] = ho[8 + ws_->c + l++];
-    TRY(comm_->allgather_host(mine.data(), 1 + kg, all.data(), s));
-    gmax = 0.0;
-    gsup.assign((size_t)kg, 0.0);
-    for (int r = 0; r < comm_->world; ++r) {
-      const double* row = all.data() + (size_t)r * (1 + kg);
-      gmax = std::max(gmax, row[0]);
-      for (int64_t t = 0; t < kg; ++t) gsup[t] += row[1 + t];
-    }
+    // each support entry lives on exactly one shard, so the rank-ordered sum of
+    // the zero-padded rows is exact
+    const double* hg = ws_->hmap + ws_->oG;
+    gmax = hg[0];
+    gsup.assign(hg + 1, hg + 1 + kg);
+    return 0;
+  }
+
+  // exchange buffers of the sharded loop (see the layout in shard_ptrs)
+  int ensure_shard_buf(int world) {
+    const int64_t kc = ws_->kcap;
+    const int64_t need = (1 + kc) * (1 + world) + 3 * kc * (1 + world) + 3 * kc * world + 1;
+    if (need <= ws_->shard_cap) return 0;
+    if (ws_->shard_buf) GI_CUDA_TRY(cudaFreeAsync(ws_->shard_buf, ws_->stream));
+    ws_->shard_buf = nullptr;
+    GI_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws_->shard_buf),
+                                sizeof(double) * (size_t)need, ws_->stream));
+    ws_->shard_cap = need;
     return 0;
   }
 
@@ -357,7 +386,7 @@ class NativeFit {
     out.clear();
     cudaStream_t s = ws_->stream;
     const int64_t ke = std::min(k, ws_->kcap);
-    std::vector<uint64_t> keys;
+    if (sharded() && ke > 0) return topk_sharded(mode, mu, ke, out, den_mu);
     if (ws_->p == 0 || k <= 0) {
       if (den_mu) TRY(sync());
     } else {
@@ -378,48 +407,59 @@ class NativeFit {
       const uint64_t* hk = reinterpret_cast<const uint64_t*>(ho + 1 + 2 * kc);
       out.resize((size_t)cnt);
       for (int64_t t = 0; t < cnt; ++t) out[t] = Pair{hi[t], ho[1 + kc + t]};
-      if (sharded()) keys.assign(hk, hk + cnt);
+      (void)hk;
     }
     if (den_mu) {
       den_mu[0] = ws_->hmap[ws_->oM];
       den_mu[1] = ws_->hmap[ws_->oM + 1];
     }
-    if (sharded() && ke > 0) TRY(merge_shards(out, keys, ke));
     std::sort(out.begin(), out.end(), [](const Pair& a, const Pair& b) { return a.idx < b.idx; });
     return 0;
   }
 
-  // Global top-k from the shards' local top-k lists: every shard's list is its
-  // exact top-k under (|value| desc, index asc), so the union holds the global
-  // one.  One all-gather of (key bits, index, value) triples, merged identically
-  // on every rank.
-  int merge_shards(std::vector<Pair>& out, const std::vector<uint64_t>& keys, int64_t ke) {
-    std::vector<double> mine((size_t)(3 * ke), 0.0), all((size_t)(3 * ke * comm_->world));
-    for (size_t t = 0; t < out.size(); ++t) {
-      memcpy(&mine[3 * t], &keys[t], 8);
-      memcpy(&mine[3 * t + 1], &out[t].idx, 8);
-      mine[3 * t + 2] = out[t].val;
+  // Global top-k of a sharded fit: every shard's local list is its exact top-k
+  // under (|value| desc, index asc), so the union holds the global one.  The
+  // lists (key bits | index | value, empty slots keyed 0) are all-gathered on
+  // the device and merged there by the same select, straight into mapped host
+  // memory -- one host sync.  Every rank takes part, empty shards included.
+  int topk_sharded(int mode, double mu, int64_t ke, std::vector<Pair>& out, double* den_mu) {
+    cudaStream_t s = ws_->stream;
+    const int world = comm_->world;
+    const int64_t kc = ws_->kcap;
+    TRY(ensure_shard_buf(world));
+    double* loc = ws_->shard_buf + (1 + kc) * (1 + world);
+    double* allc = loc + 3 * kc;
+    uint64_t* ckey = reinterpret_cast<uint64_t*>(allc + 3 * kc * world);
+    int64_t* cidx = reinterpret_cast<int64_t*>(ckey + kc * world);
+    double* cval = reinterpret_cast<double*>(cidx + kc * world);
+    int64_t* lcount = reinterpret_cast<int64_t*>(cval + kc * world);
+    GI_CUDA_TRY(cudaMemsetAsync(loc, 0, sizeof(double) * 3 * ke, s));  // key 0 = empty slot
+    if (ws_->p > 0) {
+      TRY(gi::launch_topk(ws_->p, ke, mode, ws_->beta, ws_->g, mu, j_base_, ws_->ckey, ws_->cidx,
+                          ws_->cval, reinterpret_cast<int64_t*>(loc + ke), loc + 2 * ke,
+                          reinterpret_cast<uint64_t*>(loc), lcount, s,
+                          den_mu ? ws_->scal + 5 : nullptr, ws_->ticket));
+      ++launches;
     }
-    TRY(comm_->allgather_host(mine.data(), 3 * ke, all.data(), ws_->stream));
-    struct Cand {
-      uint64_t key;
-      int64_t idx;
-      double val;
-    };
-    std::vector<Cand> cands;
-    for (size_t e = 0; e < all.size(); e += 3) {
-      Cand c;
-      memcpy(&c.key, &all[e], 8);
-      memcpy(&c.idx, &all[e + 1], 8);
-      c.val = all[e + 2];
-      if (c.key != 0) cands.push_back(c);  // 0 marks an empty slot
+    TRY(comm_->allgather_device(loc, 3 * ke, allc, s));
+    double* dm = ws_->dmap + ws_->oT;
+    TRY(gi::launch_shard_merge(world, ke, allc, ckey, cidx, cval,
+                               reinterpret_cast<int64_t*>(dm + 1), dm + 1 + kc,
+                               reinterpret_cast<uint64_t*>(dm + 1 + 2 * kc),
+                               reinterpret_cast<int64_t*>(dm), s));
+    launches += 2;
+    TRY(sync());
+    const double* ho = ws_->hmap + ws_->oT;
+    int64_t cnt = 0;
+    memcpy(&cnt, ho, sizeof(int64_t));
+    const int64_t* hi = reinterpret_cast<const int64_t*>(ho + 1);
+    out.resize((size_t)cnt);
+    for (int64_t t = 0; t < cnt; ++t) out[t] = Pair{hi[t], ho[1 + kc + t]};
+    if (den_mu) {
+      den_mu[0] = ws_->hmap[ws_->oM];
+      den_mu[1] = ws_->hmap[ws_->oM + 1];
     }
-    std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
-      return a.key != b.key ? a.key > b.key : a.idx < b.idx;
-    });
-    if ((int64_t)cands.size() > ke) cands.resize((size_t)ke);
-    out.clear();
-    for (const Cand& c : cands) out.push_back(Pair{c.idx, c.val});
+    std::sort(out.begin(), out.end(), [](const Pair& a, const Pair& b) { return a.idx < b.idx; });
     return 0;
   }
 

@@ -726,6 +726,76 @@ int launch_topk(int64_t p, int64_t k, int mode, const double* beta, const double
   return 0;
 }
 
+// ---------------------------------------------------------------- shard exchange
+// Device side of the sharded loop's exchanges (fit.cu, gi_fit_sharded).
+// mine = [max|g| (scal[3]), g[gsel[t]] or 0 for each global support entry t]
+__global__ void shard_gather_kernel(int64_t kg, const int64_t* __restrict__ gsel,
+                                    const double* __restrict__ g,
+                                    const double* __restrict__ scal3,
+                                    double* __restrict__ mine) {
+  if (threadIdx.x == 0) mine[0] = *scal3;
+  for (int64_t t = threadIdx.x; t < kg; t += blockDim.x)
+    mine[1 + t] = gsel[t] >= 0 ? g[gsel[t]] : 0.0;
+}
+
+// out = [max over ranks of all[r][0], sum over ranks of all[r][1 + t]], ranks in
+// order (the same operations as the host fold it replaces)
+__global__ void shard_fold_kernel(int world, int64_t kg, const double* __restrict__ all,
+                                  double* __restrict__ out) {
+  const int64_t row = 1 + kg;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int r = 0; r < world; ++r) m = fmax(m, all[r * row]);
+    out[0] = m;
+  }
+  for (int64_t t = threadIdx.x; t < kg; t += blockDim.x) {
+    double acc = 0.0;
+    for (int r = 0; r < world; ++r) acc += all[r * row + 1 + t];
+    out[1 + t] = acc;
+  }
+}
+
+// rank-major [key | idx | val] x world -> contiguous candidate arrays
+__global__ void shard_cands_kernel(int world, int64_t ke, const double* __restrict__ all,
+                                   uint64_t* __restrict__ ckey, int64_t* __restrict__ cidx,
+                                   double* __restrict__ cval) {
+  const int64_t total = (int64_t)world * ke;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ke, s2 = e - r * ke;
+    const double* base = all + r * 3 * ke;
+    ckey[e] = (uint64_t)__double_as_longlong(base[s2]);
+    cidx[e] = (int64_t)__double_as_longlong(base[ke + s2]);
+    cval[e] = base[2 * ke + s2];
+  }
+}
+
+int launch_shard_gather(int64_t kg, const int64_t* gsel, const double* g, const double* scal3,
+                        double* mine, cudaStream_t s) {
+  shard_gather_kernel<<<1, 256, 0, s>>>(kg, gsel, g, scal3, mine);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_shard_fold(int world, int64_t kg, const double* all, double* out, cudaStream_t s) {
+  shard_fold_kernel<<<1, 256, 0, s>>>(world, kg, all, out);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_shard_merge(int world, int64_t ke, const double* all, uint64_t* ckey, int64_t* cidx,
+                       double* cval, int64_t* out_idx, double* out_val, uint64_t* out_key,
+                       int64_t* out_count, cudaStream_t s) {
+  const int64_t total = (int64_t)world * ke;
+  shard_cands_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(world, ke, all, ckey, cidx,
+                                                                     cval);
+  GI_LAUNCH_CHECK();
+  topk_merge_kernel<<<1, kTopkThreads, 0, s>>>(total, ke, ckey, cidx, cval, out_idx, out_val,
+                                               out_key, out_count);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
 // dense beta update: beta[idx[t]] = val[t]
 __global__ void scatter_kernel(int64_t k, const int64_t* __restrict__ idx,
                                const double* __restrict__ val, double* __restrict__ beta) {
