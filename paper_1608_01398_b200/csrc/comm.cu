@@ -86,37 +86,6 @@ int gi_comm::allreduce_device(double* dbuf, int64_t count, int op, cudaStream_t 
   return 0;
 }
 
-int gi_comm::allgather_host(const double* send, int64_t count, double* recv, cudaStream_t s) {
-  if (kind == kCallbacks) {
-    if (world <= 1) {
-      memcpy(recv, send, sizeof(double) * count);
-      return 0;
-    }
-    if (allgather(ctx, send, count, recv) != 0) {
-      gi_set_error("host all-gather callback failed");
-      return -1;
-    }
-    return 0;
-  }
-  // NCCL: stage through the communicator's device scratch
-  const int64_t need = count * (world + 1);
-  if (need > scratch_doubles) {
-    if (scratch) cudaFree(scratch);
-    scratch = nullptr;
-    GI_CUDA_TRY(cudaMalloc(&scratch, sizeof(double) * need));
-    scratch_doubles = need;
-  }
-  double* dsend = scratch;
-  double* drecv = scratch + count;
-  GI_CUDA_TRY(cudaMemcpyAsync(dsend, send, sizeof(double) * count, cudaMemcpyHostToDevice, s));
-  NCCL_TRY(nccl().all_gather(dsend, drecv, (size_t)count, ncclFloat64,
-                             static_cast<ncclComm_t>(nccl_comm), s));
-  GI_CUDA_TRY(cudaMemcpyAsync(recv, drecv, sizeof(double) * count * world, cudaMemcpyDeviceToHost,
-                              s));
-  GI_CUDA_TRY(cudaStreamSynchronize(s));
-  return 0;
-}
-
 int gi_comm::allgather_device(const double* dsend, int64_t count, double* drecv,
                               cudaStream_t s) {
   if (count <= 0) return 0;
@@ -145,7 +114,6 @@ int gi_comm::allgather_device(const double* dsend, int64_t count, double* drecv,
 }
 
 gi_comm::~gi_comm() {
-  if (scratch) cudaFree(scratch);
   if (kind == kNccl && nccl_comm && nccl().ready)
     nccl().comm_destroy(static_cast<ncclComm_t>(nccl_comm));
 }

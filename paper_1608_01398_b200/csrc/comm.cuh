@@ -14,15 +14,11 @@ struct gi_comm {
   void* ctx = nullptr;
   gi_comm_allreduce_fn allreduce = nullptr;
   gi_comm_allgather_fn allgather = nullptr;
-  double* scratch = nullptr;
-  int64_t scratch_doubles = 0;
 
   // in-place all-reduce of a device buffer on stream s (op 0 = sum, 1 = max)
   int allreduce_device(double* dbuf, int64_t count, int op, cudaStream_t s);
-  // all-gather of host buffers: recv = world x count, rank-major
-  int allgather_host(const double* send, int64_t count, double* recv, cudaStream_t s);
-  // all-gather of device buffers on stream s (NCCL: in the stream, no host
-  // sync; callbacks: staged through the host)
+  // all-gather of device buffers on stream s, recv = world x count rank-major
+  // (NCCL: in the stream, no host sync; callbacks: staged through the host)
   int allgather_device(const double* dsend, int64_t count, double* drecv, cudaStream_t s);
   ~gi_comm();
 };
