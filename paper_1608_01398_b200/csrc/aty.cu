@@ -106,7 +106,10 @@ struct FastArgs {
   const double* scal;    // [1] = mean of r used for centring, [2] = sum of rt
   double scale;
   double* out;
-  int64_t n_items;
+  int64_t n_items;        // n_chunks x n_slices
+  int64_t n_slices;       // tile slices per group chunk (1: an item covers every tile)
+  double* part;           // n_slices > 1: per-slice partial sums, [slice][G * 32]
+  unsigned int* cticket;  // n_slices > 1: per-chunk arrival counters (zero between launches)
   unsigned long long* gmax;  // optional: atomicMax of |out_j| (bits of a non-negative double)
   // optional: the last CTA to finish copies these segments (gradient entries
   // included, read through L2) into pub_out -- mapped host memory of the
@@ -355,15 +358,19 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
   for (int s2 = 0; s2 < kSlots; ++s2) uses[s2] = 0;
 
   for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
-    const int64_t g0 = item * m.G / a.n_items;
-    const int64_t g1 = (item + 1) * m.G / a.n_items;
+    // item = (chunk of SNP groups, slice of sample tiles)
+    const int64_t S = a.n_slices, C = a.n_items / S;
+    const int64_t chunk = item / S, slice = item - chunk * S;
+    const int64_t g0 = chunk * m.G / C;
+    const int64_t g1 = (chunk + 1) * m.G / C;
+    const int64_t t0 = slice * m.T / S, t1 = (slice + 1) * m.T / S;
     const uint32_t ng = (uint32_t)(g1 - g0);
     const uint8_t* xitem = m.x + block_offset(0, g0, m.G);
     const bool has_work = (uint32_t)warp < ng;
     GI_ASSERT(ng <= (uint32_t)kMaxGroups && g1 <= m.G);
 
     // copy issuer: lane 0 keeps kSlots blocks of this warp's stream in flight
-    BlockCursor issue{(uint32_t)warp, (uint32_t)warp, ng, 0, m.T};
+    BlockCursor issue{(uint32_t)warp, (uint32_t)warp, ng, t0, t1};
     int next_slot = 0;
     auto issue_one = [&]() {
       if (issue.valid()) {
@@ -387,11 +394,11 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
 
     for (uint32_t gl = warp; gl < ng; gl += kWarps) acc[gl * 32 + lane] = 0.0;
     for (uint32_t gl = tid; gl < ng; gl += kThreads) gflag[gl] = a.group_missing[g0 + gl];
-    float4 r_next = load_tile_r(a.rt, 0, tid);
-    for (int64_t t = 0; t < m.T; ++t) {
+    float4 r_next = load_tile_r(a.rt, t0, tid);
+    for (int64_t t = t0; t < t1; ++t) {
       __syncthreads();  // previous tile's lookups are done
       build_table(tbl, r_next, tid);
-      if (t + 1 < m.T) r_next = load_tile_r(a.rt, t + 1, tid);  // hidden behind the tile
+      if (t + 1 < t1) r_next = load_tile_r(a.rt, t + 1, tid);  // hidden behind the tile
       __syncthreads();
       for (uint32_t gl = warp; gl < ng; gl += kWarps) {
         // wait for this slot's next phase (strictly in order: never ambiguous)
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         for (int s2 = 0; s2 < kSlots; ++s2)
           if (s2 == cur_slot) u0 = uses[s2];
         mbar_wait(bar0 + 8 * cur_slot, u0 & 1);
-        GI_ASSERT(gl < ng && t < m.T);
+        GI_ASSERT(gl < ng && t < t1);
         uint32_t wd[32];
         uint32_t sa = 0;
 #pragma unroll
@@ -429,6 +436,31 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         acc[gl * 32 + lane] += add;
       }
     }
+    // Tile slices: every slice stores its partial sums; the last slice of the
+    // chunk to arrive adds them in slice order (the same for every column, so
+    // identical columns still get identical bits) and runs the epilogue.
+    bool epilogue = true;
+    if (S > 1) {
+      const int64_t stride = m.G * 32;
+      for (uint32_t gl = warp; gl < ng; gl += kWarps)
+        a.part[slice * stride + (g0 + gl) * 32 + lane] = acc[gl * 32 + lane];
+      __threadfence();
+      __syncthreads();
+      int last = 0;
+      if (tid == 0) last = atomicAdd(a.cticket + chunk, 1u) == (unsigned)(S - 1);
+      epilogue = __syncthreads_or(last);
+      if (epilogue) {
+        __threadfence();
+        for (uint32_t gl = warp; gl < ng; gl += kWarps) {
+          double sum = 0.0;
+          for (int64_t s2 = 0; s2 < S; ++s2)
+            sum += __ldcg(a.part + s2 * stride + (g0 + gl) * 32 + lane);
+          acc[gl * 32 + lane] = sum;
+        }
+        if (tid == 0) a.cticket[chunk] = 0u;
+      }
+    }
+    if (epilogue) {
     // epilogue: out_j = scale * v_j * (acc_j - u_j * sum_rt + mean * (s1_j - u_j cnt_j));
     // the last term restores the constant part of r removed by centring (zero
     // up to rounding when u_j is the mean over the same rows; not for
@@ -453,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
       if (lane == 0)
         atomicMax(a.gmax, (unsigned long long)__double_as_longlong(local_max));
     }
+    }  // epilogue
     __syncthreads();  // accumulators, flags and table are reused by the next item
   }
   if (a.pub_ticket) {
@@ -475,11 +508,57 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
   }
 }
 
+// Work decomposition of aty_fast_kernel: `chunks` ranges of at most kMaxGroups
+// SNP groups times `slices` ranges of sample tiles.  Each (item, tile) builds
+// a 128 KiB table, so items should be as wide in groups as the accumulators
+// allow; when p is small (few groups per SM) the tiles are split instead.
+// Chosen to minimise the modelled per-SM LSU work: per item and tile, 20 KiB
+// per group (4 KiB staged + 16 KiB of table reads) plus the 128 KiB build,
+// times the rounds of items over the SMs.  With `sliced` false (no partial
+// buffer) only single-slice plans are considered.
+void aty_fast_plan(const MatrixDesc& m, int num_sms, bool sliced, int64_t& chunks,
+                   int64_t& slices) {
+  const int64_t G = m.G, T = m.T, sms = num_sms;
+  auto cost = [&](int64_t c, int64_t s) {
+    const int64_t rounds = (c * s + sms - 1) / sms;
+    const int64_t tiles = (T + s - 1) / s;
+    const int64_t groups = (G + c - 1) / c;
+    return (double)rounds * (double)tiles * (20.0 * (double)groups + 128.0);
+  };
+  const int64_t per_wave = sms * kMaxGroups;
+  chunks = sms * ((G + per_wave - 1) / per_wave);
+  if (chunks > G) chunks = G;
+  if (chunks < 1) chunks = 1;
+  slices = 1;
+  if (!sliced || G >= per_wave) return;
+  double best = cost(chunks, 1);
+  const int64_t cmin = (G + kMaxGroups - 1) / kMaxGroups;
+  for (int64_t s2 = 2; s2 <= T && s2 <= 64; ++s2) {
+    const int64_t cands[3] = {cmin, sms / s2, (sms + s2 - 1) / s2};
+    for (int64_t c : cands) {
+      if (c < cmin || c > G || c * s2 > 2 * sms) continue;
+      const double v = cost(c, s2);
+      if (v < best) {
+        best = v;
+        chunks = c;
+        slices = s2;
+      }
+    }
+  }
+}
+
+int64_t aty_fast_part_doubles(const MatrixDesc& m, int num_sms) {
+  int64_t c = 0, s2 = 1;
+  aty_fast_plan(m, num_sms, true, c, s2);
+  return s2 > 1 ? s2 * m.G * 32 : 0;
+}
+
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
                     const double* u, const double* v, const int32_t* s1cnt,
                     const double* d_scal, double scale, double* out, int num_sms,
                     cudaStream_t s, double* d_gmax, const PubArgs* pub,
-                    unsigned int* pub_ticket, void* pub_out) {
+                    unsigned int* pub_ticket, void* pub_out, double* part,
+                    unsigned int* cticket) {
   if (m.p == 0) return 0;
 
   static std::once_flag once;
@@ -508,9 +587,18 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
     a.pub_ticket = nullptr;
     a.pub_out = nullptr;
   }
-  const int64_t per_wave = (int64_t)num_sms * kMaxGroups;
-  int64_t items = (int64_t)num_sms * ((m.G + per_wave - 1) / per_wave);
-  if (items > m.G) items = m.G;
+  int64_t chunks = 0, slices = 1;
+  aty_fast_plan(m, num_sms, part != nullptr, chunks, slices);
+  if (slices > 1) {
+    GI_ASSERT(part && cticket);
+    a.part = part;
+    a.cticket = cticket;
+  } else {
+    a.part = nullptr;
+    a.cticket = nullptr;
+  }
+  a.n_slices = slices;
+  const int64_t items = chunks * slices;
   a.n_items = items;
   const int grid = (int)(items < num_sms ? items : num_sms);
   aty_fast_kernel<<<grid, kThreads, kSmemFast, s>>>(a);

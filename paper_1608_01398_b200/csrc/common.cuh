@@ -175,7 +175,13 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
                     const double* u, const double* v, const int32_t* s1cnt,
                     const double* d_scal, double scale, double* out, int num_sms,
                     cudaStream_t s, double* d_gmax = nullptr, const PubArgs* pub = nullptr,
-                    unsigned int* pub_ticket = nullptr, void* pub_out = nullptr);
+                    unsigned int* pub_ticket = nullptr, void* pub_out = nullptr,
+                    double* part = nullptr, unsigned int* cticket = nullptr);
+// X^T r work decomposition (aty.cu) and the partial-sum buffer it needs when
+// tiles are sliced (0: single-slice plan); chunk tickets: at most 2 * num_sms
+void aty_fast_plan(const MatrixDesc& m, int num_sms, bool sliced, int64_t& chunks,
+                   int64_t& slices);
+int64_t aty_fast_part_doubles(const MatrixDesc& m, int num_sms);
 int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u,
                      const double* v, const double* d_sum_r, double scale, double* out,
                      cudaStream_t s);

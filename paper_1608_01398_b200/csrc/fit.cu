@@ -45,6 +45,8 @@ struct FitWs {
   int32_t* s1cnt = nullptr;
   uint32_t *ticket = nullptr, *rowmask = nullptr;
   uint64_t* ckey = nullptr;
+  double* aty_part = nullptr;      // X^T r tile-slice partial sums (small p only)
+  uint32_t* aty_ticket = nullptr;  // X^T r per-chunk arrival counters
   int64_t* cidx = nullptr;
   double* cval = nullptr;
   // uploads: pinned host arena mirrored byte for byte by a device arena
@@ -136,6 +138,14 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   TRY(ws->dalloc(ws->ckey, ws->slots));
   TRY(ws->dalloc(ws->cidx, ws->slots));
   TRY(ws->dalloc(ws->cval, ws->slots));
+  {
+    const int64_t part = gi::aty_fast_part_doubles(h->desc(), h->sms);
+    if (part > 0) {
+      TRY(ws->dalloc(ws->aty_part, part));
+      TRY(ws->dalloc(ws->aty_ticket, 2 * (int64_t)h->sms));
+      GI_CUDA_TRY(cudaMemsetAsync(ws->aty_ticket, 0, sizeof(uint32_t) * 2 * h->sms, ws->stream));
+    }
+  }
   // between two syncs a phase stages at most ~3 sparse vectors of <= 2 kcap
   // entries plus one covariate vector; the arena is reset at every sync
   ws->in_cap = (size_t)(128 * kcap + 64) * sizeof(double);
@@ -286,7 +296,7 @@ class NativeFit {
       TRY(gi::launch_aty_fast(d, static_cast<const uint8_t*>(h_->gmiss->ptr), ws_->rt, ws_->u,
                               ws_->v, ws_->s1cnt, ws_->scal, -1.0, ws_->g, h_->sms, s,
                               ws_->scal + 3,  // max|g| fused into the epilogue
-                              &pub, ws_->ticket, ws_->dmap));
+                              &pub, ws_->ticket, ws_->dmap, ws_->aty_part, ws_->aty_ticket));
       if (ev1) GI_CUDA_TRY(cudaEventRecord(ev1, s));
       ++aty_launches;
       ++launches;
