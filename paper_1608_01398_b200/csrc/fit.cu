@@ -514,6 +514,7 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
                     const double* v, const gi_fit_config* cfg, const int64_t* warm_idx,
                     const double* warm_w, int64_t warm_k, const double* bcov0,
                     gi_fit_result* res) {
+  const auto t_start = std::chrono::steady_clock::now();
   CHECK_ARG(h && cfg && res, "NULL argument");
   CHECK_ARG(c >= 0 && c <= 64, "the native loop supports at most 64 covariate columns");
   CHECK_ARG(c == 0 || C != nullptr, "covariate matrix is NULL");
@@ -798,8 +799,12 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   res->reason = reason;
   res->backtracks = total_bt;
   if (getenv("GI_TRACE_FIT"))
-    fprintf(stderr, "gi_fit: %lld iterations, %d syncs, %.1f us waiting in sync, %d launches\n",
-            (long long)iterations, F.syncs, F.sync_us, F.launches);
+    fprintf(stderr,
+            "gi_fit: %lld iterations, %d syncs, %.1f us waiting in sync, %d launches, "
+            "%.1f us in gi_fit\n",
+            (long long)iterations, F.syncs, F.sync_us, F.launches,
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start)
+                .count());
   res->kernel_launches = F.launches;
   res->aty_ms_total = F.aty_ms;
   res->aty_launches = F.aty_launches;

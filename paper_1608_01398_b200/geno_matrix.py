@@ -368,6 +368,20 @@ class CovariateBlock:
     def subset_rows(self, rows) -> "CovariateBlock":
         return CovariateBlock(values=self.values[np.asarray(rows)], labels=self.labels)
 
+    def least_squares(self, y) -> np.ndarray:
+        """The minimum-norm least-squares coefficients of y on the block -- the
+        reference's ``np.linalg.lstsq(C, y, rcond=None)`` (iht.py:208) -- through
+        a pseudo-inverse cached on the (immutable) block with lstsq's rank
+        cutoff (eps * max(n, c) * sigma_max): one (c, n) x n product per fit
+        instead of an SVD of C (2 ms at n = 100k), equal to lstsq's solution up
+        to rounding."""
+        pinv = self.__dict__.get("_pinv")
+        if pinv is None:
+            n, c = self.values.shape
+            pinv = np.linalg.pinv(self.values, rtol=np.finfo(np.float64).eps * max(n, c))
+            object.__setattr__(self, "_pinv", pinv)
+        return pinv @ np.asarray(y, dtype=np.float64)
+
 
 @dataclass(frozen=True, eq=False)
 class StandardizedView:
