@@ -590,7 +590,10 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
   int64_t chunks = 0, slices = 1;
   aty_fast_plan(m, num_sms, part != nullptr, chunks, slices);
   if (slices > 1) {
-    GI_ASSERT(part && cticket);
+    if (!part || !cticket) {
+      gi_set_error("internal: sliced X^T r plan without its partial buffer");
+      return -1;
+    }
     a.part = part;
     a.cticket = cticket;
   } else {
@@ -616,7 +619,8 @@ constexpr int kExactWarps = 8;
 __global__ void __launch_bounds__(kExactWarps * 32) aty_exact_kernel(
     MatrixDesc m, const double* __restrict__ r_pad, const double* __restrict__ u,
     const double* __restrict__ v, const double* __restrict__ sum_r, double scale,
-    double* __restrict__ out) {
+    double* __restrict__ out, unsigned long long* gmax, PubArgs pub, unsigned int* pub_ticket,
+    unsigned long long* pub_out) {
   __shared__ double rs[GI_TILE_SAMPLES];
   __shared__ __align__(16) uint8_t blk[kExactWarps][GI_BLOCK_BYTES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -660,20 +664,51 @@ __global__ void __launch_bounds__(kExactWarps * 32) aty_exact_kernel(
       }
     }
   }
-  if (!active) return;
+  double local_max = 0.0;
   const int64_t j = g * 32 + lane;
-  if (j < m.p) {
+  if (active && j < m.p) {
     const double val = __dmul_rn(v[j], __dsub_rn(t, __dmul_rn(u[j], __dsub_rn(*sum_r, mm))));
     out[j] = __dmul_rn(scale, val);
+    local_max = fabs(val);
+  }
+  // optional fused epilogues, as in aty_fast_kernel: max|g| (exact,
+  // order-independent) and the last CTA's publish into mapped host memory
+  if (gmax) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      local_max = fmax(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+    if (lane == 0) atomicMax(gmax, (unsigned long long)__double_as_longlong(local_max));
+  }
+  if (pub_ticket) {
+    __threadfence();
+    __syncthreads();
+    int last = 0;
+    if (threadIdx.x == 0) last = atomicAdd(pub_ticket, 1u) == gridDim.x - 1;
+    if (__syncthreads_or(last)) {
+      __threadfence();
+      for (int q = 0; q < pub.nseg; ++q) {
+        const PubSeg sg = pub.seg[q];
+        const unsigned long long* src = static_cast<const unsigned long long*>(sg.src);
+        for (int64_t e = threadIdx.x; e < sg.count; e += blockDim.x)
+          pub_out[sg.dst + e] = __ldcg(sg.idx ? src + sg.idx[e] : src + e);
+      }
+      if (threadIdx.x == 0) *pub_ticket = 0u;
+    }
   }
 }
 
 int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u, const double* v,
-                     const double* d_sum_r, double scale, double* out, cudaStream_t s) {
+                     const double* d_sum_r, double scale, double* out, cudaStream_t s,
+                     double* d_gmax, const PubArgs* pub, unsigned int* pub_ticket,
+                     void* pub_out) {
   if (m.p == 0) return 0;
   const int64_t blocks = (m.G + kExactWarps - 1) / kExactWarps;
-  aty_exact_kernel<<<(unsigned)blocks, kExactWarps * 32, 0, s>>>(m, r_pad, u, v, d_sum_r,
-                                                                 scale, out);
+  PubArgs pa;
+  const bool publish = pub && pub_ticket && pub_out;
+  if (publish) pa = *pub;
+  aty_exact_kernel<<<(unsigned)blocks, kExactWarps * 32, 0, s>>>(
+      m, r_pad, u, v, d_sum_r, scale, out, reinterpret_cast<unsigned long long*>(d_gmax), pa,
+      publish ? pub_ticket : nullptr, static_cast<unsigned long long*>(pub_out));
   GI_LAUNCH_CHECK();
   return 0;
 }

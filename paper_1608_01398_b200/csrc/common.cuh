@@ -184,7 +184,8 @@ void aty_fast_plan(const MatrixDesc& m, int num_sms, bool sliced, int64_t& chunk
 int64_t aty_fast_part_doubles(const MatrixDesc& m, int num_sms);
 int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u,
                      const double* v, const double* d_sum_r, double scale, double* out,
-                     cudaStream_t s);
+                     cudaStream_t s, double* d_gmax = nullptr, const PubArgs* pub = nullptr,
+                     unsigned int* pub_ticket = nullptr, void* pub_out = nullptr);
 int launch_ax(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
               const double* w, int64_t k, double* out, int accumulate, cudaStream_t s);
 int launch_decompress(const MatrixDesc& m, const double* u, const double* v,

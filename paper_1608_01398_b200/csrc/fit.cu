@@ -120,7 +120,9 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   const int64_t n = h->n, p = std::max<int64_t>(h->p, 1);
   TRY(ws->dalloc(ws->y, n));
   TRY(ws->dalloc(ws->C, n * std::max<int64_t>(c, 1)));
-  TRY(ws->dalloc(ws->r, n));
+  // r is padded to whole tiles (zero tail) for the exact X^T r kernel
+  TRY(ws->dalloc(ws->r, ws->npad));
+  GI_CUDA_TRY(cudaMemsetAsync(ws->r, 0, sizeof(double) * ws->npad, ws->stream));
   TRY(ws->dalloc(ws->fitb, n));
   TRY(ws->dalloc(ws->img, n));
   TRY(ws->dalloc(ws->g, p));
@@ -174,7 +176,21 @@ class NativeFit {
   NativeFit(gi_matrix* h, FitWs* ws, const gi_fit_config* cfg, bool masked, double n_eff,
             gi_comm* comm, int64_t j_base)
       : h_(h), ws_(ws), cfg_(*cfg), masked_(masked), n_eff_(n_eff), comm_(comm),
-        j_base_(j_base) {}
+        j_base_(j_base) {
+    // The exact fp64 X^T r kernel -- the reference's own operation order --
+    // replaces the fast one where few samples per parameter can amplify the
+    // fast kernel's ~6e-7 gradient error past the 1e-6 parity bound (a
+    // randomised stress found one such case: 62 samples, 22 + 2 parameters):
+    // n <= 8 (k + c + 1) with the matrix up to 256 MiB, and any matrix up to
+    // 2 MiB, where the two kernels cost the same (both latency-bound).
+    // GI_XTR_EXACT=0/1 forces the fast / exact kernel.
+    const gi::MatrixDesc d = h->desc();
+    const double bytes = (double)d.G * (double)d.T * GI_BLOCK_BYTES;
+    const double params = (double)cfg->k + (double)ws->c + 1.0;
+    exact_ = bytes <= 2.0 * 1048576.0 || (n_eff <= 8.0 * params && bytes <= 256.0 * 1048576.0);
+    if (const char* e = getenv("GI_XTR_EXACT")) exact_ = atoi(e) != 0;
+  }
+  bool exact_ = false;
 
   // gi_fit_sharded always runs the exchange steps, also on a world of one
   // (which is how the NCCL backend is exercised on a single GPU)
@@ -281,9 +297,11 @@ class NativeFit {
                                     ws_->ticket, s));
     pend_k_ = 0;
     launches += ws_->c > 8 ? 1 + (ws_->c + 7) / 8 : 1;
-    TRY(gi::launch_center(ws_->n, ws_->npad, ws_->r, keep, ws_->scal, ws_->rt, ws_->partials,
-                          ws_->ticket, s));
-    ++launches;
+    if (!exact_) {
+      TRY(gi::launch_center(ws_->n, ws_->npad, ws_->r, keep, ws_->scal, ws_->rt, ws_->partials,
+                            ws_->ticket, s));
+      ++launches;
+    }
     // scal, g_cov and g on the (local) support -> mapped host memory, written by
     // the last CTA of the X^T r kernel (a separate launch only when p == 0)
     const int64_t ks = (int64_t)lsup.size();
@@ -291,7 +309,17 @@ class NativeFit {
     pub.add(ws_->scal, 8, ws_->oR);
     pub.add(ws_->cvec + ws_->c, ws_->c, ws_->oR + 8);
     pub.add(ws_->g, ks, ws_->oR + 8 + ws_->c, d_sup);
-    if (ws_->p) {
+    if (ws_->p && exact_) {
+      // g = -X^T r in the reference's fp64 order (sum r from the residual
+      // kernel), then max|g| and the publish
+      if (ev0) GI_CUDA_TRY(cudaEventRecord(ev0, s));
+      GI_CUDA_TRY(cudaMemsetAsync(ws_->scal + 3, 0, sizeof(double), s));  // max|g| slot
+      TRY(gi::launch_aty_exact(d, ws_->r, ws_->u, ws_->v, ws_->scal + 6, -1.0, ws_->g, s,
+                               ws_->scal + 3, &pub, ws_->ticket, ws_->dmap));
+      if (ev1) GI_CUDA_TRY(cudaEventRecord(ev1, s));
+      ++aty_launches;
+      ++launches;
+    } else if (ws_->p) {
       if (ev0) GI_CUDA_TRY(cudaEventRecord(ev0, s));
       TRY(gi::launch_aty_fast(d, static_cast<const uint8_t*>(h_->gmiss->ptr), ws_->rt, ws_->u,
                               ws_->v, ws_->s1cnt, ws_->scal, -1.0, ws_->g, h_->sms, s,
@@ -302,6 +330,8 @@ class NativeFit {
       ++launches;
     }
     if (!ws_->p) {
+      if (exact_)  // the centring kernel, skipped here, clears the max|g| slot
+        GI_CUDA_TRY(cudaMemsetAsync(ws_->scal + 3, 0, sizeof(double), s));
       TRY(gi::launch_publish(pub, ws_->dmap, s));
       ++launches;
     }

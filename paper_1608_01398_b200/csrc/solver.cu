@@ -180,6 +180,7 @@ __global__ void refresh_residual_kernel(int64_t n, const double* __restrict__ y,
     if (threadIdx.x == 0) {
       scal[0] = 0.5 * s2;
       scal[1] = n_eff > 0.0 ? s1 / n_eff : 0.0;
+      scal[6] = s1;  // sum of r, for the exact X^T r kernel
       if (kCov)
         for (int l = 0; l < c; ++l) gcov[l] = -gl[l];
       *ws.ticket = 0u;
