@@ -519,6 +519,9 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
 void aty_fast_plan(const MatrixDesc& m, int num_sms, bool sliced, int64_t& chunks,
                    int64_t& slices) {
   const int64_t G = m.G, T = m.T, sms = num_sms;
+  chunks = 1;
+  slices = 1;
+  if (G <= 0 || T <= 0 || sms <= 0) return;  // nothing to sweep (an empty shard)
   auto cost = [&](int64_t c, int64_t s) {
     const int64_t rounds = (c * s + sms - 1) / sms;
     const int64_t tiles = (T + s - 1) / s;
@@ -536,7 +539,7 @@ void aty_fast_plan(const MatrixDesc& m, int num_sms, bool sliced, int64_t& chunk
   for (int64_t s2 = 2; s2 <= T && s2 <= 64; ++s2) {
     const int64_t cands[3] = {cmin, sms / s2, (sms + s2 - 1) / s2};
     for (int64_t c : cands) {
-      if (c < cmin || c > G || c * s2 > 2 * sms) continue;
+      if (c < 1 || c < cmin || c > G || c * s2 > 2 * sms) continue;
       const double v = cost(c, s2);
       if (v < best) {
         best = v;

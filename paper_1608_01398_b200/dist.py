@@ -14,6 +14,8 @@ tests).
 
 from __future__ import annotations
 
+import traceback
+
 import numpy as np
 
 
@@ -140,6 +142,7 @@ class NativeComm:
                     arr[:] = comm.allreduce_host(arr.copy(), "sum" if op == 0 else "max")
                     return 0
                 except Exception:  # reported by the library as a failed collective
+                    traceback.print_exc()
                     return -1
 
             def allgather(_ctx, send, count, recv):
@@ -149,6 +152,7 @@ class NativeComm:
                     dst[:] = np.concatenate(comm.allgather_host(src))
                     return 0
                 except Exception:
+                    traceback.print_exc()
                     return -1
 
             # keep the ctypes thunks alive as long as the communicator

@@ -136,3 +136,52 @@ def test_nccl_backend_world_one_matches_device_fit():
         np.testing.assert_allclose(weights, want.model.weights, rtol=1e-6)
         np.testing.assert_allclose(covar, want.model.covar, rtol=1e-6, atol=1e-12)
         np.testing.assert_allclose(trace, want.loss_trace, rtol=1e-6)
+
+
+def _empty_shard_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1608_01398_b200 as gi
+        from paper_1608_01398_b200.dist import ShardedGenotypes, TorchComm
+
+        torch.cuda.set_device(0)
+        codes = oracle.random_codes(400, 300, seed=13, missing_rate=0.02)
+        j0, j1 = (0, 300) if rank == 0 else (300, 300)  # rank 1 owns no SNPs
+        geno = ShardedGenotypes(gi.PackedGenotypeMatrix.from_codes(codes[:, j0:j1]), j0, 300,
+                                TorchComm())
+        view = gi.StandardizedView(geno, gi.CovariateBlock.build(None, n=400))
+        y = oracle.OraclePacked.from_codes(codes).ax_columns(np.array([4, 99]),
+                                                            np.array([1.0, -1.0]))
+        res = gi.fit(view, y, gi.IhtConfig(k=3))
+        q.put((rank, res.model.support, res.iterations))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_fit_with_an_empty_shard():
+    """A rank that owns no SNPs still takes part in every exchange (its X^T r
+    plan, top-k and gather are empty) and the fit matches the unsharded one."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_empty_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    out = sorted([q.get(timeout=600) for _ in range(2)], key=lambda t: t[0])
+    for p_ in procs:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    import paper_1608_01398_b200 as gi
+
+    codes = oracle.random_codes(400, 300, seed=13, missing_rate=0.02)
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    y = oracle.OraclePacked.from_codes(codes).ax_columns(np.array([4, 99]), np.array([1.0, -1.0]))
+    want = gi.fit(gi.StandardizedView(m, gi.CovariateBlock.build(None, n=400)), y,
+                  gi.IhtConfig(k=3))
+    for _, support, iters in out:
+        np.testing.assert_array_equal(support, want.model.support)
+        assert iters == want.iterations
