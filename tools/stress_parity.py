@@ -5,6 +5,7 @@ masked CV folds and duplicated columns (exact ties in the top-k).  Prints one
 line per mismatch and a summary; exit code 1 on any mismatch.
 
     python tools/stress_parity.py [cases] [seed0]
+    GI_STRESS_LARGE=1 python tools/stress_parity.py ...   # larger shapes (fast kernel)
 """
 import os
 import sys
@@ -28,8 +29,52 @@ def rel(a, b):
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
 
 
+LARGE = os.environ.get("GI_STRESS_LARGE") == "1"  # n up to 20k, p up to 120k: fast-kernel plans
+
+
+def build_large(seed):
+    """Larger problems from the device generator and its CPU twin (same bytes,
+    no dense code matrix on the host): the fast kernel's multi-item and
+    tile-sliced work plans, masked folds, covariates, warm starts."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2000, 20000))
+    p = int(rng.integers(5000, 120000))
+    miss = float(rng.choice([0.0, 0.0, 0.02]))
+    m = gi.PackedGenotypeMatrix.synthetic(n, p, seed, missing_rate=miss)
+    ref_p = oracle.OraclePacked.from_bed(oracle.synth_bed(seed, n, 0, p, missing=miss), n)
+    c_extra = int(rng.choice([0, 0, 2]))
+    covar = rng.standard_normal((n, c_extra)) if c_extra else None
+    block = gi.CovariateBlock.build(covar, n=n)
+    k = int(rng.integers(1, 40))
+    support = np.sort(rng.choice(p, int(rng.integers(1, 12)), replace=False))
+    y = ref_p.ax_columns(support, rng.standard_normal(support.size)) \
+        + rng.normal(0, float(rng.choice([0.05, 0.5])), n)
+    warm = None
+    if rng.random() < 0.2:
+        widx = np.sort(rng.choice(p, min(k, 3), replace=False))
+        warm = (widx, rng.standard_normal(widx.size), np.zeros(block.c))
+    keep = np.flatnonzero(rng.random(n) < 0.8) if rng.random() < 0.25 else None
+    if keep is not None:
+        u, v = m.masked_stats(np.isin(np.arange(n), keep).astype(np.uint8))
+        ref_view = oracle.OracleView(ref_p.subset_rows(keep), block.values[keep])
+        view = gi.StandardizedView(FoldGenotypes(m.with_stats(u, v), keep),
+                                   block.subset_rows(keep))
+        y_fit = y[keep]
+    else:
+        ref_view = oracle.OracleView(ref_p, block.values)
+        view = gi.StandardizedView(m, block)
+        y_fit = y
+    warm_model = None if warm is None else \
+        gi.SparseModel.from_parts(warm[0], warm[1], warm[2], k=k, p=p)
+    desc = f"seed={seed} n={n} p={p} k={k} miss={miss} c={block.c} " \
+           f"masked={keep is not None} warm={warm is not None} (large)"
+    return view, ref_view, y_fit, k, warm, warm_model, desc
+
+
 def build(seed):
     """The random problem of `seed`: device view, oracle view, response, budget, warm start."""
+    if LARGE:
+        return build_large(seed)
     rng = np.random.default_rng(seed)
     n = int(rng.integers(20, 2500))
     p = int(rng.integers(5, 6000))
