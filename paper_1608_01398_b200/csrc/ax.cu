@@ -12,15 +12,35 @@
 // subtraction, as in the reference), then each genotype costs one table read
 // and one fp64 add.
 #include "common.cuh"
+#include "reduce.cuh"
 
 namespace gi {
 
 constexpr int kAxMaxCols = 1024;
 
+// kNorm: instead of storing X_S w, reduce its image norm in the same pass --
+// sum over the kept rows of (x_i + C_i wc)^2 with the per-element operations of
+// image_sumsq_kernel (add_cov, mask, square) -- and let the last block write
+// scal[slot], optionally scal[ratio_out] = ratio_num / scal[slot] and the
+// mapped pair host_out = {scal[slot], ratio} (the native loop's image phase).
+struct AxNorm {
+  const double* C;
+  int c;
+  const double* wc;
+  const uint8_t* keep;
+  double* scal;
+  int slot;
+  int ratio_out;
+  double ratio_num;
+  double* host_out;
+  RedWs ws;
+};
+
+template <bool kNorm>
 __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
                           const double* __restrict__ v, const int64_t* __restrict__ idx,
                           const double* __restrict__ w, int k, double* __restrict__ out,
-                          int accumulate) {
+                          int accumulate, AxNorm nm) {
   __shared__ double terms[kAxMaxCols][4];
   __shared__ int64_t cols[kAxMaxCols];
   __shared__ int live[kAxMaxCols];
@@ -41,6 +61,7 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
   // a thread per 16-sample word left most SMs idle.  Each sample still adds the
   // columns' terms in the caller's order (same bits as _ax_cols_kernel).
   const int64_t nbytes = (m.n + 3) / 4;
+  double nacc[1] = {0.0};
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbytes;
        b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i0 = b * 4;
@@ -72,9 +93,46 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
         }
       }
     }
+    if (!kNorm) {
 #pragma unroll
-    for (int s = 0; s < 4; ++s)
-      if (s < cnt) out[i0 + s] = acc[s];
+      for (int s = 0; s < 4; ++s)
+        if (s < cnt) out[i0 + s] = acc[s];
+    } else {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        if (s >= cnt) continue;
+        double xi = acc[s];
+        if (nm.c > 0) {
+          double cb = 0.0;
+          for (int l = 0; l < nm.c; ++l)
+            cb = __dadd_rn(cb, __dmul_rn(nm.C[(i0 + s) * nm.c + l], nm.wc[l]));
+          xi = __dadd_rn(xi, cb);
+        }
+        if (nm.keep && !nm.keep[i0 + s]) xi = 0.0;
+        nacc[0] += xi * xi;
+      }
+    }
+  }
+  if (kNorm) {
+    __shared__ double sh[32];
+    block_sum<1>(nacc, sh);
+    if (threadIdx.x == 0) nm.ws.partials[blockIdx.x] = nacc[0];
+    if (last_block(nm.ws.ticket) && threadIdx.x < 32) {
+      const double sum = fold_sum(nm.ws.partials, 1, 0, gridDim.x);
+      if (threadIdx.x == 0) {
+        nm.scal[nm.slot] = sum;
+        double ratio = 0.0;
+        if (nm.ratio_out >= 0) {
+          ratio = nm.ratio_num / sum;
+          nm.scal[nm.ratio_out] = ratio;
+        }
+        if (nm.host_out) {
+          nm.host_out[0] = sum;
+          nm.host_out[1] = ratio;
+        }
+        *nm.ws.ticket = 0u;
+      }
+    }
   }
 }
 
@@ -91,10 +149,27 @@ int launch_ax(const MatrixDesc& m, const double* u, const double* v, const int64
   }
   for (int64_t c0 = 0; c0 < k; c0 += kAxMaxCols) {
     const int kc = (int)((k - c0) < kAxMaxCols ? (k - c0) : kAxMaxCols);
-    ax_kernel<<<(unsigned)blocks, threads, 0, s>>>(m, u, v, idx + c0, w + c0, kc, out,
-                                                    (accumulate || c0 > 0) ? 1 : 0);
+    ax_kernel<false><<<(unsigned)blocks, threads, 0, s>>>(m, u, v, idx + c0, w + c0, kc, out,
+                                                           (accumulate || c0 > 0) ? 1 : 0,
+                                                           AxNorm{});
     GI_LAUNCH_CHECK();
   }
+  return 0;
+}
+
+int launch_ax_norm(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
+                   const double* w, int64_t k, const double* C, int c, const double* wc,
+                   const uint8_t* keep, double* scal, int slot, int ratio_out, double ratio_num,
+                   double* host_out, double* partials, unsigned int* ticket, cudaStream_t s) {
+  if (k > kAxMaxCols || m.n == 0) return -2;  // caller falls back to ax + image_sumsq
+  const int64_t nbytes = (m.n + 3) / 4;
+  const int threads = 128;
+  int64_t blocks = (nbytes + threads - 1) / threads;
+  if (blocks > 2 * kRedBlocks) blocks = 2 * kRedBlocks;  // partials: <= 16 * kRedBlocks
+  const AxNorm nm{C, c, wc, keep, scal, slot, ratio_out, ratio_num, host_out,
+                  RedWs{partials, ticket}};
+  ax_kernel<true><<<(unsigned)blocks, threads, 0, s>>>(m, u, v, idx, w, (int)k, nullptr, 0, nm);
+  GI_LAUNCH_CHECK();
   return 0;
 }
 

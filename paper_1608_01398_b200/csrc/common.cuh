@@ -188,6 +188,12 @@ int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u,
                      unsigned int* pub_ticket = nullptr, void* pub_out = nullptr);
 int launch_ax(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
               const double* w, int64_t k, double* out, int accumulate, cudaStream_t s);
+// X_S w fused with its image norm (see ax.cu, AxNorm); returns -2 when k is
+// too large for one launch (the caller then runs launch_ax + image_sumsq)
+int launch_ax_norm(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
+                   const double* w, int64_t k, const double* C, int c, const double* wc,
+                   const uint8_t* keep, double* scal, int slot, int ratio_out, double ratio_num,
+                   double* host_out, double* partials, unsigned int* ticket, cudaStream_t s);
 int launch_decompress(const MatrixDesc& m, const double* u, const double* v,
                       const int64_t* idx, int64_t k, double* out_t, cudaStream_t s);
 }  // namespace gi

@@ -400,6 +400,18 @@ class NativeFit {
     const bool cov = wcov && ws_->c;
     if (cov) TRY(stage(wcov->data(), ws_->c, d_cov));
     TRY(flush());
+    if (!sharded()) {
+      // X_idx w and its image norm in one launch (the n-vector is never stored)
+      const int rc = gi::launch_ax_norm(d, ws_->u, ws_->v, d_idx, d_w, (int64_t)li.size(),
+                                        cov ? ws_->C : nullptr, cov ? (int)ws_->c : 0, d_cov,
+                                        masked_ ? ws_->keep : nullptr, ws_->scal, 4, ratio_out,
+                                        ratio_num, host_out, ws_->partials, ws_->ticket, s);
+      if (rc == 0) {
+        ++launches;
+        return 0;
+      }
+      if (rc != -2) return -1;  // -2: too many columns for one launch, use two kernels
+    }
     TRY(gi::launch_ax(d, ws_->u, ws_->v, d_idx, d_w, (int64_t)li.size(), ws_->img, 0, s));
     ++launches;
     if (sharded()) TRY(comm_->allreduce_device(ws_->img, ws_->n, 0, s));

@@ -111,9 +111,10 @@ def _nccl_worker(port, q):
 
 def test_nccl_backend_world_one_matches_device_fit():
     """The NCCL communicator of the native sharded loop (dlopen'd libnccl,
-    in-place device all-reduce, device-staged all-gather) on a world of one:
+    in-place device all-reduce, device all-gathers) on a world of one:
     gi_fit_sharded runs every exchange step through real NCCL collectives and
-    must reproduce the unsharded gi_fit bit for bit."""
+    must reproduce the unsharded gi_fit (to 1e-12: only the image norm's
+    summation order differs)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     proc = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
@@ -130,9 +131,10 @@ def test_nccl_backend_world_one_matches_device_fit():
     for native, (support, weights, covar, trace, iters, reason) in out.items():
         np.testing.assert_array_equal(support, want.model.support)
         assert iters == want.iterations and reason == want.reason
-        if native:  # same kernels, same order: identical bits
-            np.testing.assert_array_equal(weights, want.model.weights)
-            np.testing.assert_array_equal(trace, want.loss_trace)
+        if native:  # same kernels except the image norm's summation order (the
+            # sharded loop all-reduces X_S w before the norm; gi_fit fuses them)
+            np.testing.assert_allclose(weights, want.model.weights, rtol=1e-12, atol=0)
+            np.testing.assert_allclose(trace, want.loss_trace, rtol=1e-12, atol=0)
         np.testing.assert_allclose(weights, want.model.weights, rtol=1e-6)
         np.testing.assert_allclose(covar, want.model.covar, rtol=1e-6, atol=1e-12)
         np.testing.assert_allclose(trace, want.loss_trace, rtol=1e-6)
