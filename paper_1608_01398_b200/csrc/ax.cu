@@ -36,11 +36,38 @@ struct AxNorm {
   RedWs ws;
 };
 
-template <bool kNorm>
+// kRes (the native loop's refresh, unsharded): with f = X_S w, write the
+// residual r_i = keep_i ? y_i - (f_i + C_i b_cov) : 0 and reduce loss, sum r
+// and (c <= 8) g_cov = -C^T r -- refresh_residual_kernel's per-element
+// operations -- plus the pending beta writes (block 0).
+struct AxRes {
+  const double* y;
+  const double* C;
+  int c;
+  const double* bcov;
+  const uint8_t* keep;
+  double n_eff;
+  double* r;
+  double* scal;
+  double* gcov;  // NULL: no covariate gradient here
+  int64_t sk;
+  const int64_t* sidx;
+  const double* sval;
+  double* beta;
+  RedWs ws;
+};
+
+enum AxMode { kAxStore = 0, kAxNorm = 1, kAxRes = 2 };
+
+template <int kMode>
 __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
                           const double* __restrict__ v, const int64_t* __restrict__ idx,
                           const double* __restrict__ w, int k, double* __restrict__ out,
-                          int accumulate, AxNorm nm) {
+                          int accumulate, AxNorm nm, AxRes rs) {
+  constexpr bool kNorm = kMode == kAxNorm;
+  constexpr bool kRes = kMode == kAxRes;
+  if (kRes && blockIdx.x == 0)
+    for (int64_t t = threadIdx.x; t < rs.sk; t += blockDim.x) rs.beta[rs.sidx[t]] = rs.sval[t];
   __shared__ double terms[kAxMaxCols][4];
   __shared__ int64_t cols[kAxMaxCols];
   __shared__ int live[kAxMaxCols];
@@ -62,6 +89,10 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
   // columns' terms in the caller's order (same bits as _ax_cols_kernel).
   const int64_t nbytes = (m.n + 3) / 4;
   double nacc[1] = {0.0};
+  constexpr int kRv = 10;  // kRes reductions: r^2, r, 8 covariate columns
+  double racc[kRes ? kRv : 1];
+#pragma unroll
+  for (int q = 0; q < (kRes ? kRv : 1); ++q) racc[q] = 0.0;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbytes;
        b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i0 = b * 4;
@@ -93,10 +124,34 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
         }
       }
     }
-    if (!kNorm) {
+    if (kMode == kAxStore) {
 #pragma unroll
       for (int s = 0; s < 4; ++s)
         if (s < cnt) out[i0 + s] = acc[s];
+    } else if constexpr (kRes) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        if (s >= cnt) continue;
+        const int64_t i = i0 + s;
+        double ri = 0.0;
+        if (!rs.keep || rs.keep[i]) {
+          double f = acc[s];
+          if (rs.c > 0) {
+            double cb = 0.0;
+            for (int l = 0; l < rs.c; ++l) cb = __dadd_rn(cb, __dmul_rn(rs.C[i * rs.c + l], rs.bcov[l]));
+            f = k > 0 ? __dadd_rn(f, cb) : cb;
+          }
+          ri = __dsub_rn(rs.y[i], f);
+        }
+        rs.r[i] = ri;
+        racc[0] += ri * ri;
+        racc[1] += ri;
+        if (rs.gcov) {
+#pragma unroll
+          for (int l = 0; l < 8; ++l)
+            if (l < rs.c) racc[2 + l] += rs.C[i * rs.c + l] * ri;
+        }
+      }
     } else {
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
@@ -110,6 +165,27 @@ __global__ void ax_kernel(MatrixDesc m, const double* __restrict__ u,
         }
         if (nm.keep && !nm.keep[i0 + s]) xi = 0.0;
         nacc[0] += xi * xi;
+      }
+    }
+  }
+  if constexpr (kRes) {
+    __shared__ double shr[kRv * 32];
+    block_sum<kRv>(racc, shr);
+    if (threadIdx.x == 0)
+      for (int q = 0; q < kRv; ++q) rs.ws.partials[blockIdx.x * kRv + q] = racc[q];
+    if (last_block(rs.ws.ticket) && threadIdx.x < 32) {
+      const double s2 = fold_sum(rs.ws.partials, kRv, 0, gridDim.x);
+      const double s1 = fold_sum(rs.ws.partials, kRv, 1, gridDim.x);
+      double gl[8];
+      if (rs.gcov)
+        for (int l = 0; l < rs.c; ++l) gl[l] = fold_sum(rs.ws.partials, kRv, 2 + l, gridDim.x);
+      if (threadIdx.x == 0) {
+        rs.scal[0] = 0.5 * s2;
+        rs.scal[1] = rs.n_eff > 0.0 ? s1 / rs.n_eff : 0.0;
+        rs.scal[6] = s1;
+        if (rs.gcov)
+          for (int l = 0; l < rs.c; ++l) rs.gcov[l] = -gl[l];
+        *rs.ws.ticket = 0u;
       }
     }
   }
@@ -149,9 +225,9 @@ int launch_ax(const MatrixDesc& m, const double* u, const double* v, const int64
   }
   for (int64_t c0 = 0; c0 < k; c0 += kAxMaxCols) {
     const int kc = (int)((k - c0) < kAxMaxCols ? (k - c0) : kAxMaxCols);
-    ax_kernel<false><<<(unsigned)blocks, threads, 0, s>>>(m, u, v, idx + c0, w + c0, kc, out,
-                                                           (accumulate || c0 > 0) ? 1 : 0,
-                                                           AxNorm{});
+    ax_kernel<kAxStore><<<(unsigned)blocks, threads, 0, s>>>(m, u, v, idx + c0, w + c0, kc, out,
+                                                              (accumulate || c0 > 0) ? 1 : 0,
+                                                              AxNorm{}, AxRes{});
     GI_LAUNCH_CHECK();
   }
   return 0;
@@ -168,7 +244,27 @@ int launch_ax_norm(const MatrixDesc& m, const double* u, const double* v, const 
   if (blocks > 2 * kRedBlocks) blocks = 2 * kRedBlocks;  // partials: <= 16 * kRedBlocks
   const AxNorm nm{C, c, wc, keep, scal, slot, ratio_out, ratio_num, host_out,
                   RedWs{partials, ticket}};
-  ax_kernel<true><<<(unsigned)blocks, threads, 0, s>>>(m, u, v, idx, w, (int)k, nullptr, 0, nm);
+  ax_kernel<kAxNorm><<<(unsigned)blocks, threads, 0, s>>>(m, u, v, idx, w, (int)k, nullptr, 0, nm,
+                                                          AxRes{});
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_ax_residual(const MatrixDesc& m, const double* u, const double* v,
+                       const int64_t* idx, const double* w, int64_t k, const double* y,
+                       const double* C, int c, const double* bcov, const uint8_t* keep,
+                       double n_eff, double* r, double* scal, double* gcov, int64_t sk,
+                       const int64_t* sidx, const double* sval, double* beta, double* partials,
+                       unsigned int* ticket, cudaStream_t s) {
+  if (k > kAxMaxCols || c > 8 || m.n == 0) return -2;  // caller uses the two-kernel path
+  const int64_t nbytes = (m.n + 3) / 4;
+  const int threads = 128;
+  int64_t blocks = (nbytes + threads - 1) / threads;
+  if (blocks > kRedBlocks) blocks = kRedBlocks;  // partials: 10 per block
+  const AxRes rs{y, C, c, bcov, keep, n_eff, r, scal, c > 0 ? gcov : nullptr, sk, sidx, sval,
+                 beta, RedWs{partials, ticket}};
+  ax_kernel<kAxRes><<<(unsigned)blocks, threads, 0, s>>>(m, u, v, idx, w, (int)k, nullptr, 0,
+                                                         AxNorm{}, rs);
   GI_LAUNCH_CHECK();
   return 0;
 }

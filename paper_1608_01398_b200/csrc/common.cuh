@@ -194,6 +194,14 @@ int launch_ax_norm(const MatrixDesc& m, const double* u, const double* v, const 
                    const double* w, int64_t k, const double* C, int c, const double* wc,
                    const uint8_t* keep, double* scal, int slot, int ratio_out, double ratio_num,
                    double* host_out, double* partials, unsigned int* ticket, cudaStream_t s);
+// X_S w fused with the refresh's residual, loss, sum r, g_cov (c <= 8) and the
+// pending beta writes; -2 when k or c is too large (two-kernel path instead)
+int launch_ax_residual(const MatrixDesc& m, const double* u, const double* v,
+                       const int64_t* idx, const double* w, int64_t k, const double* y,
+                       const double* C, int c, const double* bcov, const uint8_t* keep,
+                       double n_eff, double* r, double* scal, double* gcov, int64_t sk,
+                       const int64_t* sidx, const double* sval, double* beta, double* partials,
+                       unsigned int* ticket, cudaStream_t s);
 int launch_decompress(const MatrixDesc& m, const double* u, const double* v,
                       const int64_t* idx, int64_t k, double* out_t, cudaStream_t s);
 }  // namespace gi

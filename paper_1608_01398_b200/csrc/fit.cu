@@ -281,22 +281,39 @@ class NativeFit {
       TRY(stage(gsel.data(), kg, d_gsel));
     }
     TRY(flush());
-    if (has_fit) {
-      TRY(gi::launch_ax(d, ws_->u, ws_->v, d_sup, d_w, (int64_t)lsup.size(), ws_->fitb, 0, s));
-      ++launches;
-      // X_S b summed over the shards (NCCL in place on this stream)
-      if (sharded()) TRY(comm_->allreduce_device(ws_->fitb, ws_->n, 0, s));
-    }
-    // residual + loss + mean, the pending beta writes and g_cov = -C^T r in one
-    // kernel (g_cov in a second one only beyond 8 covariates)
     const uint8_t* keep = masked_ ? ws_->keep : nullptr;
-    TRY(gi::launch_refresh_residual(ws_->n, ws_->y, has_fit ? ws_->fitb : nullptr,
-                                    ws_->c ? ws_->C : nullptr, (int)ws_->c, d_cov, keep, n_eff_,
-                                    ws_->r, ws_->scal, ws_->c ? ws_->cvec + ws_->c : nullptr,
-                                    pend_k_, pend_idx_, pend_w_, ws_->beta, ws_->partials,
-                                    ws_->ticket, s));
-    pend_k_ = 0;
-    launches += ws_->c > 8 ? 1 + (ws_->c + 7) / 8 : 1;
+    int fused = -2;
+    if (!sharded()) {
+      // X_S b, residual, loss, sum r, g_cov and the pending beta writes in one
+      // kernel (the fitted values are never stored)
+      fused = gi::launch_ax_residual(d, ws_->u, ws_->v, d_sup, d_w, (int64_t)lsup.size(), ws_->y,
+                                     ws_->c ? ws_->C : nullptr, (int)ws_->c, d_cov, keep, n_eff_,
+                                     ws_->r, ws_->scal, ws_->c ? ws_->cvec + ws_->c : nullptr,
+                                     pend_k_, pend_idx_, pend_w_, ws_->beta, ws_->partials,
+                                     ws_->ticket, s);
+      if (fused != 0 && fused != -2) return -1;
+      if (fused == 0) {
+        pend_k_ = 0;
+        ++launches;
+      }
+    }
+    if (fused != 0) {
+      if (has_fit) {
+        TRY(gi::launch_ax(d, ws_->u, ws_->v, d_sup, d_w, (int64_t)lsup.size(), ws_->fitb, 0, s));
+        ++launches;
+        // X_S b summed over the shards (NCCL in place on this stream)
+        if (sharded()) TRY(comm_->allreduce_device(ws_->fitb, ws_->n, 0, s));
+      }
+      // residual + loss + mean, the pending beta writes and g_cov = -C^T r in one
+      // kernel (g_cov in a second one only beyond 8 covariates)
+      TRY(gi::launch_refresh_residual(ws_->n, ws_->y, has_fit ? ws_->fitb : nullptr,
+                                      ws_->c ? ws_->C : nullptr, (int)ws_->c, d_cov, keep,
+                                      n_eff_, ws_->r, ws_->scal,
+                                      ws_->c ? ws_->cvec + ws_->c : nullptr, pend_k_, pend_idx_,
+                                      pend_w_, ws_->beta, ws_->partials, ws_->ticket, s));
+      pend_k_ = 0;
+      launches += ws_->c > 8 ? 1 + (ws_->c + 7) / 8 : 1;
+    }
     if (!exact_) {
       TRY(gi::launch_center(ws_->n, ws_->npad, ws_->r, keep, ws_->scal, ws_->rt, ws_->partials,
                             ws_->ticket, s));
