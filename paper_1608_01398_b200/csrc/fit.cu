@@ -258,7 +258,7 @@ class NativeFit {
   // _refresh_state: returns loss, max|g|, g_cov, g on the support
   int refresh(const std::vector<int64_t>& sup, const std::vector<double>& w,
               const std::vector<double>& bcov, double& loss, double& gmax,
-              std::vector<double>& gcov, std::vector<double>& gsup) {
+              std::vector<double>& gcov, std::vector<double>& gsup, bool need_grad = true) {
     const gi::MatrixDesc d = h_->desc();
     cudaStream_t s = ws_->stream;
     const bool has_fit = !sup.empty();
@@ -313,6 +313,23 @@ class NativeFit {
                                       pend_w_, ws_->beta, ws_->partials, ws_->ticket, s));
       pend_k_ = 0;
       launches += ws_->c > 8 ? 1 + (ws_->c + 7) / 8 : 1;
+    }
+    if (!need_grad) {
+      // the fit ends after this refresh (converged or max_iter): the reference
+      // computes g here but FitResult never reads it (iht.py:326-355), so only
+      // the residual's loss and g_cov come back
+      gi::PubArgs pub;
+      pub.add(ws_->scal, 8, ws_->oR);
+      pub.add(ws_->cvec + ws_->c, ws_->c, ws_->oR + 8);
+      TRY(gi::launch_publish(pub, ws_->dmap, s));
+      ++launches;
+      TRY(sync());
+      const double* ho = ws_->hmap + ws_->oR;
+      loss = ho[0];
+      gmax = 0.0;
+      gcov.assign(ho + 8, ho + 8 + ws_->c);
+      gsup.clear();
+      return 0;
     }
     if (!exact_) {
       TRY(gi::launch_center(ws_->n, ws_->npad, ws_->r, keep, ws_->scal, ws_->rt, ws_->partials,
@@ -829,7 +846,10 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
         sup = new_sup;
         w = new_w;
         bcov = cand_cov;
-        TRY(F.refresh(sup, w, bcov, loss, gmax, gcov, gsup));
+        // the last refresh of a fit (step_inf < tol, or the final allowed
+        // iteration) needs only the loss
+        const bool last = step_inf < cfg->tol || it + 1 >= cfg->max_iter;
+        TRY(F.refresh(sup, w, bcov, loss, gmax, gcov, gsup, !last));
       }
     }
     ++iterations;
