@@ -6,6 +6,7 @@ timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_
 timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.json 2>&1; echo "ref rc=$?"
 timeout 900 python bench.py --workload c2path > gpurun_out/bench_c2path.json 2>&1; echo "c2 rc=$?"
 timeout 1200 python bench.py --workload c4cv > gpurun_out/bench_c4cv.json 2>&1; echo "c4 rc=$?"
+timeout 1500 python bench.py --workload c5 --steps 3 > gpurun_out/bench_c5.json 2>&1; echo "c5 rc=$?"
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_final.csv $CMD > gpurun_out/ncu_list.log 2>&1
