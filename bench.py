@@ -95,7 +95,7 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def smem_roofline(n, p, ms, sm_mhz, sms, missing, miss_group_frac=None):
+def smem_roofline(n, p, ms, sm_mhz, sms, missing, miss_group_frac=None, base3=False):
     """Secondary roofline of aty_fast_kernel: its shared-memory traffic against
     the SM crossbar (128 B/clk/SM, B300_MICROARCH.md "LDS/STS") at the SM clock
     sampled during the run.  LSU shared-memory traffic per byte of the tiled
@@ -109,7 +109,8 @@ def smem_roofline(n, p, ms, sm_mhz, sms, missing, miss_group_frac=None):
     such groups is known (`miss_group_frac`)."""
     if not ms or not sm_mhz:
         return None
-    T = (n + 511) // 512
+    # base-3 copy (missing-free matrices): 640-sample tiles of the same 4 KiB blocks
+    T = (n + 639) // 640 if base3 else (n + 511) // 512
     G = (p + 31) // 32
     per_wave = sms * 112  # kMaxGroups groups per work item (aty.cu)
     items = min(sms * ((G + per_wave - 1) // per_wave), G)
@@ -125,12 +126,12 @@ def smem_roofline(n, p, ms, sm_mhz, sms, missing, miss_group_frac=None):
                      if missing and miss_group_frac is None else None)}
 
 
-def traffic_from_profile(n, p):
+def traffic_from_profile(n, p, fmt):
     path = os.path.join(ROOT, "profiles", "aty_fast_traffic.json")
     try:
         with open(path) as fh:
             rec = json.load(fh)
-        if rec.get("n") == n and rec.get("p") == p:
+        if rec.get("n") == n and rec.get("p") == p and rec.get("format", "2-bit") == fmt:
             return float(rec["dram_bytes_per_launch"])
     except Exception:
         pass
@@ -549,11 +550,17 @@ def main():
     # ---- roofline of the X^T r kernel
     n, p_local = a.n, (geno.local.p if sharded else a.p)
     nb = (n + 3) // 4
-    alg_bytes = p_local * nb + 8 * n + 24 * p_local
+    # X^T r streams the base-3 copy (1.6 bits per genotype) when the matrix has
+    # no missing genotypes, else the 2-bit BED tiles: algorithmic bytes are
+    # those of the format it reads (packed X + r + u, v, s1/cnt + g)
+    base3 = (geno.local if sharded else geno).xtr_base3
+    fmt = "base-3" if base3 else "2-bit"
+    x_bytes = p_local * ((n + 4) // 5) if base3 else p_local * nb
+    alg_bytes = x_bytes + 8 * n + 24 * p_local
     aty_avg = statistics.mean(aty_ms) if aty_ms else float("nan")
     achieved = alg_bytes / (aty_avg / 1e3) / 1e9
     peak, peak_kind = measured_peak()
-    traffic = traffic_from_profile(n, p_local)
+    traffic = traffic_from_profile(n, p_local, fmt)
 
     cpu = None
     if world == 1 and not a.no_cpu:
@@ -578,15 +585,19 @@ def main():
         # smallest are below the noise, so not every one is recoverable)
         "planted_recovered": (f"{np.intersect1d(last.model.support, truth.support).size}"
                               f"/{truth.support.size}") if last is not None else None,
+        # BED-equivalent: 2-bit packed genotype bytes per second (above the HBM
+        # bandwidth when the kernel streams the 1.6-bit base-3 copy)
         "xtr_packed_gbs": p_local * nb / (aty_avg / 1e3) / 1e9,
         "xtr_ms": aty_avg,
+        "xtr_format": ("base-3 device copy, 5 genotypes per byte (no missing genotypes)"
+                       if base3 else "2-bit BED tiles"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "aty_fast_kernel", "bytes_per_launch": alg_bytes,
                      "smem": smem_roofline(n, p_local, aty_avg, clk.get("sm_mhz"),
                                            torch.cuda.get_device_properties(local)
                                            .multi_processor_count, a.missing,
-                                           miss_frac)},
+                                           miss_frac, base3)},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h // max(a.steps, 1)},

@@ -67,6 +67,7 @@ def _declare(lib):
         "gi_matrix_subset_rows": ([P, P, c_i64, P], c_int),
         "gi_matrix_free": ([P], c_int),
         "gi_matrix_shape": ([P, P, P, P], c_int),
+        "gi_matrix_xtr_format": ([P, c_int, P], c_int),
         "gi_matrix_stats": ([P, P, P], c_int),
         "gi_matrix_read_bed": ([P, c_i64, c_i64, P], c_int),
         "gi_matrix_missing_counts": ([P, P], c_int),

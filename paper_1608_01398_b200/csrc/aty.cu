@@ -174,6 +174,50 @@ __device__ __forceinline__ void build_table(uint32_t tbl, float4 r, int tid) {
   }
 }
 
+// Base-3 tiles (missing-free matrices, csrc/layout.cu pack3_kernel): byte
+// k of word w of a 640-sample tile packs samples 20 w + 5 k + s, s < 5, as
+// sum_s dose_s 3^s.  Same table geometry (position 4 w + k, 256-byte row per
+// byte value, 243 rows used), so the lookup loop is unchanged; each entry is
+//   ((d0 r0 + d1 r1) + d2 r2) + (d3 r3 + d4 r4)
+// from 27 low and 9 high partial sums (one add per entry).
+struct R5 {
+  float r[5];
+};
+
+__device__ __forceinline__ R5 load_tile_r3(const float* __restrict__ rt, int64_t t, int tid,
+                                           int64_t n) {
+  const int w = tid & 31;
+  const int k = (tid >> 5) & 3;
+  const int64_t i0 = t * GI_TILE3_SAMPLES + 20 * w + 5 * k;
+  R5 v;
+#pragma unroll
+  for (int s = 0; s < 5; ++s) v.r[s] = i0 + s < n ? rt[i0 + s] : 0.0f;
+  return v;
+}
+
+__device__ __forceinline__ float digit_term(int d, float r) {
+  return d == 1 ? r : (d == 2 ? 2.0f * r : 0.0f);  // exact in fp32
+}
+
+__device__ __forceinline__ void build_table3(uint32_t tbl, const R5& r, int tid) {
+  const int w = tid & 31;
+  const int k = (tid >> 5) & 3;
+  const int third = tid >> 7;  // high digit pairs 3 third .. 3 third + 2
+  float lo[27];
+#pragma unroll
+  for (int c = 0; c < 27; ++c)
+    lo[c] = (digit_term(c % 3, r.r[0]) + digit_term((c / 3) % 3, r.r[1])) +
+            digit_term(c / 9, r.r[2]);
+  const uint32_t base = tbl + (k >> 1) * 65536 + (k & 1) * 128 + 4 * w;
+#pragma unroll
+  for (int hh = 0; hh < 3; ++hh) {
+    const int hi = third * 3 + hh;
+    const float hv = digit_term(hi % 3, r.r[3]) + digit_term(hi / 3, r.r[4]);
+#pragma unroll
+    for (int c = 0; c < 27; ++c) sts_f32(base + (hi * 27 + c) * 256, lo[c] + hv);
+  }
+}
+
 __device__ __forceinline__ void stage_group(uint32_t slot_lane, uint32_t (&wd)[32]) {
 #pragma unroll
   for (int q = 0; q < 32; ++q) wd[q] = lds_u32_off<0>(slot_lane + q * 128);
@@ -293,6 +337,7 @@ struct BlockCursor {
   }
 };
 
+template <bool kBase3>
 __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   // Carve shared memory so that the table starts on a 64 KiB boundary of the
@@ -334,6 +379,8 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
   const MatrixDesc& m = a.m;
+  const uint8_t* const xsrc = kBase3 ? m.x3 : m.x;
+  const int64_t mT = kBase3 ? m.T3 : m.T;
 
   // this warp's slots (global slot id = warp * kSlots + s)
   uint32_t slot_addr[kSlots];
@@ -363,9 +410,9 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
     const int64_t chunk = item / S, slice = item - chunk * S;
     const int64_t g0 = chunk * m.G / C;
     const int64_t g1 = (chunk + 1) * m.G / C;
-    const int64_t t0 = slice * m.T / S, t1 = (slice + 1) * m.T / S;
+    const int64_t t0 = slice * mT / S, t1 = (slice + 1) * mT / S;
     const uint32_t ng = (uint32_t)(g1 - g0);
-    const uint8_t* xitem = m.x + block_offset(0, g0, m.G);
+    const uint8_t* xitem = xsrc + block_offset(0, g0, m.G);
     const bool has_work = (uint32_t)warp < ng;
     GI_ASSERT(ng <= (uint32_t)kMaxGroups && g1 <= m.G);
 
@@ -377,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         if (lane == 0) {
           const uint32_t bar = bar0 + 8 * next_slot;
           mbar_expect_tx(bar, GI_BLOCK_BYTES);
-          GI_ASSERT(issue.t < m.T && issue.gl < ng);
+          GI_ASSERT(issue.t < mT && issue.gl < ng);
           bulk_g2s(slot_addr[next_slot],
                    xitem + issue.t * tile_stride + (int64_t)issue.gl * GI_BLOCK_BYTES,
                    GI_BLOCK_BYTES, bar);
@@ -393,12 +440,23 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
     int cur_slot = 0;
 
     for (uint32_t gl = warp; gl < ng; gl += kWarps) acc[gl * 32 + lane] = 0.0;
-    for (uint32_t gl = tid; gl < ng; gl += kThreads) gflag[gl] = a.group_missing[g0 + gl];
-    float4 r_next = load_tile_r(a.rt, t0, tid);
+    if (!kBase3)
+      for (uint32_t gl = tid; gl < ng; gl += kThreads) gflag[gl] = a.group_missing[g0 + gl];
+    float4 r_next;
+    R5 r5_next;
+    if constexpr (kBase3)
+      r5_next = load_tile_r3(a.rt, t0, tid, m.n);
+    else
+      r_next = load_tile_r(a.rt, t0, tid);
     for (int64_t t = t0; t < t1; ++t) {
       __syncthreads();  // previous tile's lookups are done
-      build_table(tbl, r_next, tid);
-      if (t + 1 < t1) r_next = load_tile_r(a.rt, t + 1, tid);  // hidden behind the tile
+      if constexpr (kBase3) {
+        build_table3(tbl, r5_next, tid);
+        if (t + 1 < t1) r5_next = load_tile_r3(a.rt, t + 1, tid, m.n);  // hidden behind the tile
+      } else {
+        build_table(tbl, r_next, tid);
+        if (t + 1 < t1) r_next = load_tile_r(a.rt, t + 1, tid);
+      }
       __syncthreads();
       for (uint32_t gl = warp; gl < ng; gl += kWarps) {
         // wait for this slot's next phase (strictly in order: never ambiguous)
@@ -422,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         issue_one();  // refill the slot just drained
         cur_slot = cur_slot + 1 == kSlots ? 0 : cur_slot + 1;
         float tt = 0.f, tm = 0.f;
-        const bool miss = gflag[gl] != 0;
+        const bool miss = !kBase3 && gflag[gl] != 0;
         if (miss)
           process_group<true>(wd, xb, tt, tm);
         else
@@ -550,10 +608,23 @@ void aty_fast_plan(const MatrixDesc& m, int num_sms, bool sliced, int64_t& chunk
   }
 }
 
+// The plan of the tiles the kernel streams: the base-3 copy's when present.
+static MatrixDesc plan_desc(const MatrixDesc& m) {
+  MatrixDesc pm = m;
+  if (m.x3 != nullptr) pm.T = m.T3;
+  return pm;
+}
+
+// Sized for either layout (fit workspaces are shared by matrices of one shape).
 int64_t aty_fast_part_doubles(const MatrixDesc& m, int num_sms) {
-  int64_t c = 0, s2 = 1;
+  int64_t c = 0, s2 = 1, best = 0;
   aty_fast_plan(m, num_sms, true, c, s2);
-  return s2 > 1 ? s2 * m.G * 32 : 0;
+  if (s2 > 1) best = s2 * m.G * 32;
+  MatrixDesc m3 = m;
+  m3.T = tiles3_of(m.n);
+  aty_fast_plan(m3, num_sms, true, c, s2);
+  if (s2 > 1 && s2 * m.G * 32 > best) best = s2 * m.G * 32;
+  return best;
 }
 
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,
@@ -567,8 +638,11 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
   static std::once_flag once;
   static cudaError_t cfg_err = cudaSuccess;
   std::call_once(once, [] {
-    cfg_err = cudaFuncSetAttribute(aty_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kSmemFast);
+    cfg_err = cudaFuncSetAttribute(aty_fast_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFast);
+    if (cfg_err == cudaSuccess)
+      cfg_err = cudaFuncSetAttribute(aty_fast_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFast);
   });
   GI_CUDA_TRY(cfg_err);
   FastArgs a;
@@ -591,7 +665,7 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
     a.pub_out = nullptr;
   }
   int64_t chunks = 0, slices = 1;
-  aty_fast_plan(m, num_sms, part != nullptr, chunks, slices);
+  aty_fast_plan(plan_desc(m), num_sms, part != nullptr, chunks, slices);
   if (slices > 1) {
     if (!part || !cticket) {
       gi_set_error("internal: sliced X^T r plan without its partial buffer");
@@ -607,7 +681,10 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
   const int64_t items = chunks * slices;
   a.n_items = items;
   const int grid = (int)(items < num_sms ? items : num_sms);
-  aty_fast_kernel<<<grid, kThreads, kSmemFast, s>>>(a);
+  if (m.x3 != nullptr)
+    aty_fast_kernel<true><<<grid, kThreads, kSmemFast, s>>>(a);
+  else
+    aty_fast_kernel<false><<<grid, kThreads, kSmemFast, s>>>(a);
   GI_LAUNCH_CHECK();
   return 0;
 }

@@ -39,6 +39,9 @@
 #define GI_TILE_WORDS 32
 #define GI_GROUP 32
 #define GI_BLOCK_BYTES 4096
+// base-3 copy for X^T r (missing-free matrices): 5 genotypes per byte, so a
+// 128-byte tile row holds 640 samples; same 4 KiB block swizzle
+#define GI_TILE3_SAMPLES 640
 
 namespace gi {
 
@@ -49,7 +52,13 @@ struct MatrixDesc {
   int64_t nb;         // ceil(n/4) bytes per SNP in the BED layout
   int64_t T;          // sample tiles = ceil(nb / 128)
   int64_t G;          // SNP groups = ceil(p / 32)
+  const uint8_t* x3 = nullptr;  // optional base-3 tiles (read only by X^T r)
+  int64_t T3 = 0;               // base-3 sample tiles = ceil(n / 640)
 };
+
+__host__ __device__ inline int64_t tiles3_of(int64_t n) {
+  return (n + GI_TILE3_SAMPLES - 1) / GI_TILE3_SAMPLES;
+}
 
 __host__ __device__ inline int64_t block_offset(int64_t t, int64_t g, int64_t G) {
   return (t * G + g) * (int64_t)GI_BLOCK_BYTES;
@@ -169,6 +178,7 @@ int launch_subset_rows(const MatrixDesc& src, const MatrixDesc& dst, uint8_t* x,
                        const int64_t* d_rows, cudaStream_t s);
 int launch_stats(const MatrixDesc& m, const uint32_t* d_rowmask, double* u, double* v,
                  int32_t* d_missing_cnt, int32_t* d_s1cnt, cudaStream_t s);
+int launch_pack3(const MatrixDesc& m, uint8_t* x3, cudaStream_t s);
 int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_t* flags,
                        cudaStream_t s);
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,

@@ -130,6 +130,8 @@ struct gi_matrix {
   int sms = 148;
   int64_t n = 0, p = 0, nb = 0, T = 0, G = 0;
   std::shared_ptr<DevMem> x;         // swizzled tiles (shared by with_stats copies)
+  std::shared_ptr<DevMem> x3;        // optional base-3 copy for X^T r (shared likewise)
+  int64_t T3 = 0;
   std::shared_ptr<DevMem> miss_cnt;  // int32[p]
   std::shared_ptr<DevMem> gmiss;     // uint8[G]
   std::shared_ptr<DevMem> s1cnt;     // int32[2p]: sum of dosages, observed count (all rows)
@@ -155,6 +157,8 @@ struct gi_matrix {
     d.nb = nb;
     d.T = T;
     d.G = G;
+    d.x3 = x3 ? static_cast<const uint8_t*>(x3->ptr) : nullptr;
+    d.T3 = x3 ? T3 : 0;
     return d;
   }
   double* du() const { return static_cast<double*>(u->ptr); }

@@ -224,6 +224,64 @@ int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_
   return 0;
 }
 
+// ---------------------------------------------------------------- base-3 copy
+// x3 block (t3, g) holds samples 640 t3 .. +639 of SNPs 32 g .. +31 with the
+// 2-bit blocks' swizzle (word w of SNP L at byte (L ^ w) * 128 + 4 L); byte b
+// of word w packs samples i = 640 t3 + 20 w + 5 b + s, s < 5, as
+// sum_s dose_s 3^s (<= 242), dose 0/1/2 for codes 00/10/11.  Built only when
+// no SNP has a missing genotype (code 01); samples >= n and SNPs >= p are 0.
+// One thread per output word, consecutive threads on consecutive words of a
+// row q, so the stores are coalesced; the <= 3 source words per output word
+// come from the same 2-bit tile row (L1 hits across the warp's lanes).
+__global__ void pack3_kernel(MatrixDesc m, uint8_t* __restrict__ x3) {
+  const int64_t total = m.T3 * m.G * 1024;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = e >> 10;  // = t3 * G + g
+    const int q = (int)((e >> 5) & 31), L = (int)(e & 31);
+    const int64_t t3 = blk / m.G, g = blk - t3 * m.G;
+    const int w = L ^ q;
+    const int64_t j = g * 32 + L;
+    const int64_t i0 = t3 * GI_TILE3_SAMPLES + 20 * w;  // first sample of the word
+    const int64_t w0 = i0 >> 4;                         // its 16-sample source word
+    uint32_t src[3] = {0u, 0u, 0u};
+    if (j < m.p) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int64_t sw = w0 + c;  // global 16-sample word index
+        if (sw * 16 < m.n)
+          src[c] = *reinterpret_cast<const uint32_t*>(
+              m.x + word_offset(sw >> 5, j, (int)(sw & 31), m.G));
+      }
+    }
+    uint32_t out = 0u;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      uint32_t val = 0u, mul = 1u;
+#pragma unroll
+      for (int s2 = 0; s2 < 5; ++s2) {
+        const int64_t i = i0 + 5 * b + s2;
+        const int off = (int)(i - w0 * 16);  // 0 .. 34
+        const uint32_t code = i < m.n ? (src[off >> 4] >> (2 * (off & 15))) & 3u : 0u;
+        val += (code == 2u ? 1u : (code == 3u ? 2u : 0u)) * mul;
+        mul *= 3u;
+      }
+      out |= val << (8 * b);
+    }
+    *reinterpret_cast<uint32_t*>(x3 + blk * GI_BLOCK_BYTES + q * 128 + 4 * L) = out;
+  }
+}
+
+int launch_pack3(const MatrixDesc& m, uint8_t* x3, cudaStream_t s) {
+  if (m.T3 == 0 || m.G == 0) return 0;
+  const int64_t total = m.T3 * m.G * 1024;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  pack3_kernel<<<(unsigned)blocks, 256, 0, s>>>(m, x3);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
 // ---------------------------------------------------------------- subset rows
 // dst holds m samples: sample i of dst = sample rows[i] of src.  One CTA per
 // (dst tile, SNP group), 8 warps.  Warp w builds rows q = w, w + 8, ... of the

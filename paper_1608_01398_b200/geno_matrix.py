@@ -203,6 +203,21 @@ class PackedGenotypeMatrix:
             check(lib().gi_matrix_missing_counts(self._h.raw, ptr(out)))
         return out
 
+    @property
+    def xtr_base3(self) -> bool:
+        """True when X^T r streams the device's base-3 copy (5 genotypes per
+        byte; built for matrices without missing genotypes, csrc/layout.cu)."""
+        out = ctypes.c_int(0)
+        check(lib().gi_matrix_xtr_format(self._h.raw, -1, ctypes.byref(out)))
+        return bool(out.value)
+
+    def set_xtr_base3(self, enable: bool) -> bool:
+        """Build (when possible) or drop the base-3 copy; returns xtr_base3.
+        Shared with with_stats copies of this matrix."""
+        out = ctypes.c_int(0)
+        check(lib().gi_matrix_xtr_format(self._h.raw, 1 if enable else 0, ctypes.byref(out)))
+        return bool(out.value)
+
     def to_codes(self) -> np.ndarray:
         return np.ascontiguousarray(unpack_codes(self.data, self.n).T)
 

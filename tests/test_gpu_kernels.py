@@ -210,18 +210,21 @@ def test_aty_batched_fold_residuals_with_fold_stats():
         dev.aty_batched(R, U)
 
 
-def test_fast_aty_identical_columns_get_identical_gradients():
+@pytest.mark.parametrize("miss", [0.05, 0.0])  # 0.0: the base-3 copy
+def test_fast_aty_identical_columns_get_identical_gradients(miss):
     """SNPs in perfect LD have identical columns; the reference gives them
     identical gradients, so top-k ties go to the lower index.  The fast kernel
-    sums integer table entries, so its X^T r of a column depends only on the
+    sums its table entries in an order fixed by the word positions (pairwise
+    over aligned blocks), so its X^T r of a column depends only on the
     column's codes -- not on the lane/word order it is visited in."""
     gi = _gm()
     rng = np.random.default_rng(17)
     n, half = 3000, 120
-    base = oracle.random_codes(n, half, seed=17, missing_rate=0.05)
+    base = oracle.random_codes(n, half, seed=17, missing_rate=miss)
     perm = rng.permutation(half)
     codes = np.concatenate([base, base[:, perm]], axis=1)  # column half + i == column perm[i]
     dev = gi.PackedGenotypeMatrix.from_codes(codes)
+    assert dev.xtr_base3 == (miss == 0.0)
     for _ in range(3):
         g = dev.aty_genetic(rng.standard_normal(n), mode="fast")
         np.testing.assert_array_equal(g[half:], g[perm])
@@ -234,3 +237,38 @@ def test_fast_aty_identical_columns_get_identical_gradients():
                                         oracle.intercept(n)), y, 1)
     np.testing.assert_array_equal(got.model.support, want.support)
     assert got.model.support[0] == min(perm[3], half + 3)
+
+
+@pytest.mark.parametrize("n,p", [(1, 1), (5, 33), (639, 40), (640, 64), (641, 65), (1281, 700),
+                                 (5000, 3000), (20000, 257)])
+def test_base3_copy_xtr(n, p):
+    """A matrix without missing genotypes gets the base-3 copy (5 genotypes per
+    byte, 640-sample tiles); the fast X^T r over it agrees with the reference
+    within the fast kernel's tolerance, like the 2-bit tiles' sweep, and a
+    rebuilt copy gives the same bits."""
+    rng = np.random.default_rng(n * 31 + p)
+    codes = oracle.random_codes(n, p, seed=n + 7 * p, missing_rate=0.0)
+    ref = oracle.OraclePacked.from_codes(codes)
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    assert dev.xtr_base3
+    r = rng.standard_normal(n) + 1.5
+    want = ref.aty_genetic(r)
+    scale = max(np.sqrt(np.mean(want ** 2)), 1e-300)
+    g3 = dev.aty_genetic(r, mode="fast")
+    assert np.max(np.abs(g3 - want)) <= 2e-6 * scale + 1e-12
+    assert dev.set_xtr_base3(False) is False
+    g2 = dev.aty_genetic(r, mode="fast")
+    assert np.max(np.abs(g2 - want)) <= 2e-6 * scale + 1e-12
+    assert dev.set_xtr_base3(True) is True
+    np.testing.assert_array_equal(dev.aty_genetic(r, mode="fast"), g3)
+    np.testing.assert_array_equal(dev.aty_genetic(r), want)  # exact kernel: 2-bit tiles
+
+
+def test_base3_copy_needs_missing_free_matrix():
+    codes = oracle.random_codes(700, 90, seed=5, missing_rate=0.0)
+    codes[13, 77] = 1  # one missing genotype
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    assert not dev.xtr_base3
+    assert dev.set_xtr_base3(True) is False
+    sub = dev.subset_rows(np.array([i for i in range(700) if i != 13]))
+    assert sub.xtr_base3  # the fold copy without that row has none
