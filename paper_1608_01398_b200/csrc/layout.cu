@@ -230,54 +230,70 @@ int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_
 // of word w packs samples i = 640 t3 + 20 w + 5 b + s, s < 5, as
 // sum_s dose_s 3^s (<= 242), dose 0/1/2 for codes 00/10/11.  Built only when
 // no SNP has a missing genotype (code 01); samples >= n and SNPs >= p are 0.
-// One thread per output word, consecutive threads on consecutive words of a
-// row q, so the stores are coalesced; the <= 3 source words per output word
-// come from the same 2-bit tile row (L1 hits across the warp's lanes).
-__global__ void pack3_kernel(MatrixDesc m, uint8_t* __restrict__ x3) {
-  const int64_t total = m.T3 * m.G * 1024;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t blk = e >> 10;  // = t3 * G + g
-    const int q = (int)((e >> 5) & 31), L = (int)(e & 31);
+// One CTA per output block at a time: the 2-3 source blocks holding its 640
+// samples are staged in shared memory with coalesced 16-byte loads, then lane
+// L of each warp assembles word L ^ q of SNP L from its own SNP's source words
+// (bank = L, conflict-free) and the warp stores row q of the output block.
+// The 20 codes of an output word are one 40-bit window of the source words;
+// a 1024-entry table maps each 10-bit run of 5 codes to its base-3 byte.
+constexpr int kPack3Threads = 256;
+
+__global__ void __launch_bounds__(kPack3Threads) pack3_kernel(MatrixDesc m,
+                                                              uint8_t* __restrict__ x3) {
+  __shared__ __align__(16) uint32_t src[3][1024];
+  __shared__ uint8_t lut[1024];
+  for (int v = threadIdx.x; v < 1024; v += kPack3Threads) {
+    uint32_t val = 0u, mul = 1u;
+    for (int s2 = 0; s2 < 5; ++s2) {
+      const uint32_t code = (v >> (2 * s2)) & 3u;
+      val += (code == 2u ? 1u : (code == 3u ? 2u : 0u)) * mul;
+      mul *= 3u;
+    }
+    lut[v] = (uint8_t)val;
+  }
+  const int64_t nblk = m.T3 * m.G;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int64_t t3 = blk / m.G, g = blk - t3 * m.G;
-    const int w = L ^ q;
-    const int64_t j = g * 32 + L;
-    const int64_t i0 = t3 * GI_TILE3_SAMPLES + 20 * w;  // first sample of the word
-    const int64_t w0 = i0 >> 4;                         // its 16-sample source word
-    uint32_t src[3] = {0u, 0u, 0u};
-    if (j < m.p) {
+    const int64_t s0 = t3 * GI_TILE3_SAMPLES;  // first sample of the block
+    const int64_t ta = s0 / GI_TILE_SAMPLES;   // first source tile
+    int64_t tb = (s0 + GI_TILE3_SAMPLES - 1) / GI_TILE_SAMPLES;
+    if (tb > m.T - 1) tb = m.T - 1;
+    __syncthreads();  // the lut, or the previous block's reads, are done
+    for (int c = 0; c <= (int)(tb - ta); ++c)
+      reinterpret_cast<uint4*>(src[c])[threadIdx.x] =
+          reinterpret_cast<const uint4*>(m.x + block_offset(ta + c, g, m.G))[threadIdx.x];
+    __syncthreads();
+    for (int e = threadIdx.x; e < 1024; e += kPack3Threads) {
+      const int q = e >> 5, L = e & 31, w = L ^ q;
+      const int64_t i0 = s0 + 20 * w;  // first sample of the word
+      uint32_t out = 0u;
+      if (g * 32 + L < m.p && i0 < m.n) {
+        const int rel0 = (int)(i0 - ta * GI_TILE_SAMPLES);
+        const int rw0 = rel0 >> 4, o2 = 2 * (rel0 & 15);
+        uint32_t sw[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t sw = w0 + c;  // global 16-sample word index
-        if (sw * 16 < m.n)
-          src[c] = *reinterpret_cast<const uint32_t*>(
-              m.x + word_offset(sw >> 5, j, (int)(sw & 31), m.G));
+        for (int c = 0; c < 3; ++c) {
+          const int rw = rw0 + c, tc = rw >> 5, wi = rw & 31;
+          sw[c] = tc <= (int)(tb - ta) ? src[tc][((L ^ wi) << 5) + L] : 0u;
+        }
+        const uint64_t lo = (uint64_t)sw[0] | ((uint64_t)sw[1] << 32);
+        uint64_t win = lo >> o2;
+        if (o2 > 24) win |= (uint64_t)sw[2] << (64 - o2);
+        const int64_t valid = m.n - i0 < 20 ? m.n - i0 : 20;  // samples >= n are 0
+        win &= (1ull << (2 * valid)) - 1ull;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) out |= (uint32_t)lut[(win >> (10 * b)) & 1023u] << (8 * b);
       }
+      reinterpret_cast<uint32_t*>(x3 + blk * GI_BLOCK_BYTES)[e] = out;
     }
-    uint32_t out = 0u;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      uint32_t val = 0u, mul = 1u;
-#pragma unroll
-      for (int s2 = 0; s2 < 5; ++s2) {
-        const int64_t i = i0 + 5 * b + s2;
-        const int off = (int)(i - w0 * 16);  // 0 .. 34
-        const uint32_t code = i < m.n ? (src[off >> 4] >> (2 * (off & 15))) & 3u : 0u;
-        val += (code == 2u ? 1u : (code == 3u ? 2u : 0u)) * mul;
-        mul *= 3u;
-      }
-      out |= val << (8 * b);
-    }
-    *reinterpret_cast<uint32_t*>(x3 + blk * GI_BLOCK_BYTES + q * 128 + 4 * L) = out;
   }
 }
 
 int launch_pack3(const MatrixDesc& m, uint8_t* x3, cudaStream_t s) {
   if (m.T3 == 0 || m.G == 0) return 0;
-  const int64_t total = m.T3 * m.G * 1024;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  pack3_kernel<<<(unsigned)blocks, 256, 0, s>>>(m, x3);
+  int64_t blocks = m.T3 * m.G;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  pack3_kernel<<<(unsigned)blocks, kPack3Threads, 0, s>>>(m, x3);
   GI_LAUNCH_CHECK();
   return 0;
 }
