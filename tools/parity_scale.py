@@ -63,6 +63,7 @@ def main():
     t4 = time.time()
     rec = {
         "n": a.n, "p": a.p, "k": a.k, "k_true": k_true, "missing": a.missing,
+        "xtr_format": "base-3" if m.xtr_base3 else "2-bit",
         "seed": a.seed, "pheno_seed": a.pheno_seed,
         "support_equal": bool(np.array_equal(got.model.support, want.support)),
         "iterations_gpu": got.iterations, "iterations_oracle": want.iterations,
