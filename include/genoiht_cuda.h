@@ -76,7 +76,9 @@ int gi_matrix_shape(const gi_matrix *h, int64_t *n, int64_t *p, int *device);
 /* No reference counterpart (device layout): X^T r of a matrix without missing
  * genotypes streams a base-3 copy (5 genotypes per byte, 1.6 bits) built at
  * finalize.  set = -1 queries, 0 drops the copy, 1 builds it when possible;
- * *base3 (may be NULL) receives 1 if the copy exists. */
+ * *base3 (may be NULL) receives 1 if the copy exists.  Changing the format
+ * must not overlap a fit or X^T r on the same handle (it frees or replaces
+ * the copy); with_stats copies made earlier keep the copy they share. */
 int gi_matrix_xtr_format(gi_matrix *h, int set, int *base3);
 /* u, v (host out, length p): PackedGenotypeMatrix.u / .v */
 int gi_matrix_stats(const gi_matrix *h, double *u, double *v);
