@@ -272,3 +272,19 @@ def test_base3_copy_needs_missing_free_matrix():
     assert dev.set_xtr_base3(True) is False
     sub = dev.subset_rows(np.array([i for i in range(700) if i != 13]))
     assert sub.xtr_base3  # the fold copy without that row has none
+
+
+def test_base3_copy_env_switch(monkeypatch):
+    """GI_BASE3=0 keeps X^T r on the 2-bit tiles (read when a matrix is built)."""
+    codes = oracle.random_codes(900, 70, seed=11, missing_rate=0.0)
+    monkeypatch.setenv("GI_BASE3", "0")
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    assert not dev.xtr_base3
+    monkeypatch.delenv("GI_BASE3")
+    dev2 = _gm().PackedGenotypeMatrix.from_codes(codes)
+    assert dev2.xtr_base3
+    r = np.random.default_rng(2).standard_normal(900)
+    want = oracle.OraclePacked.from_codes(codes).aty_genetic(r)
+    scale = np.sqrt(np.mean(want ** 2))
+    for m in (dev, dev2):
+        assert np.max(np.abs(m.aty_genetic(r, mode="fast") - want)) <= 2e-6 * scale + 1e-12
