@@ -53,18 +53,38 @@ __device__ __forceinline__ void block_sum(double (&x)[NV], double* sh) {
 
 // Deterministic fold of per-block partials by the first warp of the last
 // block: lane l sums partials l, l+32, ... in order, then a fixed xor tree.
+// The loop is unrolled over the grids the kernels launch (<= 2 kRedBlocks
+// blocks) with predicated loads, so a lane's loads all issue before its adds
+// instead of one L2 round trip per partial; the additions keep their order
+// (b = lane, lane + 32, ...), so the sums are the same bits as a plain loop.
+constexpr int kFoldUnroll = (2 * kRedBlocks + 31) / 32;
+
 __device__ __forceinline__ double fold_sum(const double* partials, int stride, int slot,
                                            unsigned nblocks) {
-  const int lane = threadIdx.x & 31;
+  const unsigned lane = threadIdx.x & 31;
+  double v[kFoldUnroll];
+#pragma unroll
+  for (int q = 0; q < kFoldUnroll; ++q) {
+    const unsigned b = lane + 32u * q;
+    v[q] = b < nblocks ? partials[b * stride + slot] : 0.0;
+  }
   double s = 0.0;
-  for (unsigned b = lane; b < nblocks; b += 32) s += partials[b * stride + slot];
+#pragma unroll
+  for (int q = 0; q < kFoldUnroll; ++q)
+    if (lane + 32u * q < nblocks) s += v[q];
+  for (unsigned b = lane + 32u * kFoldUnroll; b < nblocks; b += 32) s += partials[b * stride + slot];
   return warp_sum(s);
 }
 
 __device__ __forceinline__ double fold_max(const double* partials, unsigned nblocks) {
-  const int lane = threadIdx.x & 31;
+  const unsigned lane = threadIdx.x & 31;
   double s = 0.0;
-  for (unsigned b = lane; b < nblocks; b += 32) s = fmax(s, partials[b]);
+#pragma unroll
+  for (int q = 0; q < kFoldUnroll; ++q) {
+    const unsigned b = lane + 32u * q;
+    if (b < nblocks) s = fmax(s, partials[b]);
+  }
+  for (unsigned b = lane + 32u * kFoldUnroll; b < nblocks; b += 32) s = fmax(s, partials[b]);
   return warp_max(s);
 }
 
