@@ -459,6 +459,15 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
       }
       __syncthreads();
       for (uint32_t gl = warp; gl < ng; gl += kWarps) {
+        // u_j for the missing-sum term, loaded before the block wait and the
+        // lookups so its latency is hidden (issued after them it stalled the
+        // warp on the epilogue's DFMA: ~10% of the samples at 2% missing)
+        const bool miss = !kBase3 && gflag[gl] != 0;
+        double uj = 0.0;
+        if (miss) {
+          const int64_t j = (g0 + gl) * 32 + lane;
+          if (j < m.p) uj = __ldg(a.u + j);
+        }
         // wait for this slot's next phase (strictly in order: never ambiguous)
         uint32_t u0 = 0;
 #pragma unroll
@@ -480,17 +489,12 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
         issue_one();  // refill the slot just drained
         cur_slot = cur_slot + 1 == kSlots ? 0 : cur_slot + 1;
         float tt = 0.f, tm = 0.f;
-        const bool miss = !kBase3 && gflag[gl] != 0;
         if (miss)
           process_group<true>(wd, xb, tt, tm);
         else
           process_group<false>(wd, xb, tt, tm);
         double add = (double)tt;
-        if (miss) {
-          const int64_t j = (g0 + gl) * 32 + lane;
-          const double uj = j < m.p ? a.u[j] : 0.0;
-          add += uj * (double)tm;
-        }
+        if (miss) add += uj * (double)tm;
         acc[gl * 32 + lane] += add;
       }
     }
