@@ -567,8 +567,23 @@ __global__ void __launch_bounds__(kTopkThreads) topk_local_kernel(
   const int64_t lo = (int64_t)blockIdx.x * kTopkChunk;
   const int64_t hi = lo + kTopkChunk < p ? lo + kTopkChunk : p;
   const int64_t m = hi - lo;
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x)
-    keys[i] = key_of(topk_value(mode, beta, g, mu, lo + i));
+  {
+    // all of a thread's loads first, then the keys (the same operations as
+    // topk_value): a strided loop issued them one round trip at a time
+    constexpr int kPer = kTopkChunk / kTopkThreads;
+    double gv[kPer], bv[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int64_t i = threadIdx.x + (int64_t)q * kTopkThreads;
+      gv[q] = i < m ? __ldg(g + lo + i) : 0.0;
+      bv[q] = (mode != 0 && i < m) ? __ldg(beta + lo + i) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int64_t i = threadIdx.x + (int64_t)q * kTopkThreads;
+      if (i < m) keys[i] = key_of(mode == 0 ? gv[q] : __dsub_rn(bv[q], __dmul_rn(mu, gv[q])));
+    }
+  }
   if (threadIdx.x == 0) s_pos = 0u;
   __syncthreads();
   uint64_t tk;
