@@ -33,6 +33,7 @@ shards the SNPs over N ranks (NCCL); the fit size stays fixed (strong scaling).
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -126,15 +127,18 @@ def smem_roofline(n, p, ms, sm_mhz, sms, missing, miss_group_frac=None, base3=Fa
                      if missing and miss_group_frac is None else None)}
 
 
-def traffic_from_profile(n, p, fmt):
-    path = os.path.join(ROOT, "profiles", "aty_fast_traffic.json")
-    try:
-        with open(path) as fh:
-            rec = json.load(fh)
-        if rec.get("n") == n and rec.get("p") == p and rec.get("format", "2-bit") == fmt:
-            return float(rec["dram_bytes_per_launch"])
-    except Exception:
-        pass
+def traffic_from_profile(n, p, fmt, missing=0.0):
+    """DRAM bytes per aty_fast_kernel launch from the committed ncu capture of
+    this shape and format (profiles/aty_fast_traffic*.json), else None."""
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "aty_fast_traffic*.json"))):
+        try:
+            with open(path) as fh:
+                rec = json.load(fh)
+            if rec.get("n") == n and rec.get("p") == p and rec.get("format", "2-bit") == fmt \
+                    and float(rec.get("missing", 0.0)) == float(missing):
+                return float(rec["dram_bytes_per_launch"])
+        except Exception:
+            continue
     return None
 
 
@@ -560,7 +564,7 @@ def main():
     aty_avg = statistics.mean(aty_ms) if aty_ms else float("nan")
     achieved = alg_bytes / (aty_avg / 1e3) / 1e9
     peak, peak_kind = measured_peak()
-    traffic = traffic_from_profile(n, p_local, fmt)
+    traffic = traffic_from_profile(n, p_local, fmt, a.missing)
 
     cpu = None
     if world == 1 and not a.no_cpu:

@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--n", type=int, required=True)
     ap.add_argument("--p", type=int, required=True)
     ap.add_argument("--format", default="2-bit", choices=["2-bit", "base-3"])
+    ap.add_argument("--missing", type=float, default=0.0)
+    ap.add_argument("--command", default="python bench.py --steps 1 --warmup 3 --no-cpu")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "aty_fast_traffic.json"))
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], check=True,
@@ -45,9 +47,9 @@ def main():
     nb = (a.n + 3) // 4
     xb = a.p * ((a.n + 4) // 5) if a.format == "base-3" else a.p * nb
     rec = {"kernel": "gi::aty_fast_kernel",
-           "command": "python bench.py --steps 1 --warmup 3 --no-cpu (ncu --set full "
-                      "--clock-control none -k regex:aty_fast -s 5 -c 1)",
-           "n": a.n, "p": a.p, "format": a.format,
+           "command": a.command + " (ncu --set full --clock-control none -k regex:aty_fast "
+                      "-s 5 -c 1)",
+           "n": a.n, "p": a.p, "format": a.format, "missing": a.missing,
            "dram_bytes_per_launch": nbytes("dram__bytes_read.sum") +
            nbytes("dram__bytes_write.sum"),
            "algorithmic_bytes_per_launch": xb + 8 * a.n + 24 * a.p,
