@@ -83,7 +83,8 @@ def config_of(a, world):
                         f"({a.p * ((a.n + 3) // 4) / 1e9:.1f} GB packed), k={a.k}, "
                         f"k_true={a.k}, intercept covariate, missing={a.missing}",
             "n": a.n, "p": a.p, "k": a.k, "step": "one cold-start IHT fit to convergence",
-            "parallelism": f"snp-shard{world}" if world > 1 else "single-gpu",
+            "parallelism": (f"snp-shard{world}" if world > 1 or
+                            os.environ.get("GI_FORCE_SHARDED") == "1" else "single-gpu"),
             "l2": "inputs (packed X) >> 126 MB L2; no flush needed"}
 
 
