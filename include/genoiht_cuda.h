@@ -188,7 +188,10 @@ typedef struct {
   double tol;
   double c_omega;
   int64_t max_backtracks;
-  int64_t flags;  /* bit 0: time every X^T r launch with CUDA events (aty_ms_total) */
+  int64_t flags;  /* bit 0: time every X^T r launch with CUDA events (aty_ms_total);
+                     bit 1: the caller chooses the X^T r kernel (bit 2 set = the exact
+                     fp64 kernel) -- gi_fit_sharded callers pass the choice made on
+                     the GLOBAL shape so every rank and the unsharded fit agree */
 } gi_fit_config;
 
 /* FitResult (iht.py:172-180); caller-allocated arrays, capacities in *_cap */

@@ -18,10 +18,11 @@
 //   distinct table positions = 32 distinct banks.  The missing-genotype sum
 //   m_j reuses the same table: mapping missing codes (01) to het (10) and the
 //   rest to 00 makes T[b'] = sum of r over the missing slots.
-//   Blocks of the matrix (4 KiB = 32 SNPs x 512 samples) stream through a
-//   16-slot shared-memory ring filled by a producer warp with
-//   cp.async.bulk (TMA bulk copies, mbarrier complete_tx), with an L2 prefetch
-//   running ahead.  Per (SNP, tile) partial sums are fp32, summed pairwise in
+//   Blocks of the matrix (4 KiB = 32 SNPs x 512 samples) stream through one
+//   private shared-memory slot per warp: each of the 12 warps walks its own
+//   groups, lane 0 re-issues the next cp.async.bulk (TMA bulk copy, mbarrier
+//   complete_tx) as soon as the warp has copied the block to registers (after
+//   a proxy fence).  Per (SNP, tile) partial sums are fp32, summed pairwise in
 //   an order that does not depend on the lane (process_group), and promoted to
 //   an fp64 accumulator per tile: identical SNP columns get identical
 //   gradients (the reference's exact ties), and the error is <= ~6e-7 of
@@ -79,10 +80,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
           "r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
-}
-
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 
@@ -484,6 +481,10 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
 #pragma unroll
         for (int s2 = 0; s2 < kSlots; ++s2)
           if (s2 == cur_slot) ++uses[s2];
+        // the slot's generic-proxy reads above must be ordered before the
+        // async-proxy (TMA) write that refills it: proxy fence per lane, then
+        // the warp barrier, then lane 0 issues
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         next_slot = cur_slot;
         issue_one();  // refill the slot just drained

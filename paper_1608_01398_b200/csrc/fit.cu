@@ -188,6 +188,9 @@ class NativeFit {
     const double bytes = (double)d.G * (double)d.T * GI_BLOCK_BYTES;
     const double params = (double)cfg->k + (double)ws->c + 1.0;
     exact_ = bytes <= 2.0 * 1048576.0 || (n_eff <= 8.0 * params && bytes <= 256.0 * 1048576.0);
+    // sharded fits: the caller decides on the global shape (flags bits 1-2), so
+    // ranks whose shards straddle a threshold still run the same kernel
+    if (cfg->flags & 2) exact_ = (cfg->flags & 4) != 0;
     if (const char* e = getenv("GI_XTR_EXACT")) exact_ = atoi(e) != 0;
   }
   bool exact_ = false;
@@ -635,6 +638,12 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
     }
   } pool_return{pool, ws};
   cudaStream_t s = ws->stream;
+  if (ws->in_off != 0 || ws->in_flushed != 0) {
+    // a previous fit on this workspace failed between stage() and sync():
+    // drain its stream and start the staging arena afresh
+    GI_CUDA_TRY(cudaStreamSynchronize(s));
+    ws->in_off = ws->in_flushed = 0;
+  }
   const int64_t n = h->n, p = h->p;
   double n_eff = (double)n;
   const bool masked = keep != nullptr || (y == nullptr && ws->masked);

@@ -187,3 +187,120 @@ def test_sharded_fit_with_an_empty_shard():
     for _, support, iters in out:
         np.testing.assert_array_equal(support, want.model.support)
         assert iters == want.iterations
+
+
+def _path_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1608_01398_b200 as gi
+        from paper_1608_01398_b200.dist import ShardedGenotypes, TorchComm
+        from paper_1608_01398_b200.simulate import SimulationSpec, simulate_phenotype
+
+        torch.cuda.set_device(0)
+        comm = TorchComm()
+        # 1000 x 12000: 3 MiB of tiles globally (fast X^T r kernel), 1.5 MiB per
+        # shard -- each rank alone would have picked the exact kernel
+        geno = ShardedGenotypes.synthetic(1000, 12000, 31, comm, device=0)
+        view = gi.StandardizedView(geno, gi.CovariateBlock.build(None, n=1000))
+        y, _ = simulate_phenotype(view, SimulationSpec(k_true=8, seed=9))
+        # default workers (8): the path must still run its sharded fits one at a
+        # time in the same order on both ranks (one communicator per group)
+        res = gi.fit_path(view, y, [3, 8, 12])
+        q.put((rank, y, [(r.model.support, r.model.weights, r.loss_trace, r.iterations)
+                         for r in res]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fit_path_on_sharded_view_matches_unsharded_path():
+    """fit_path over an SNP-sharded view (2 ranks, gloo callbacks, one GPU):
+    its fits share the process group's communicator, so they must run
+    sequentially; and the X^T r kernel is chosen on the global shape, so the
+    shards (1.5 MiB each) run the same fast kernel as the unsharded 3 MiB fit
+    -- weights and losses agree to 1e-12 (only the image norm's summation
+    order differs)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_path_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    out = sorted([q.get(timeout=600) for _ in range(2)], key=lambda t: t[0])
+    for p_ in procs:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    import paper_1608_01398_b200 as gi
+
+    y = out[0][1]
+    full = gi.PackedGenotypeMatrix.synthetic(1000, 12000, 31)
+    want = gi.fit_path(gi.StandardizedView(full, gi.CovariateBlock.build(None, n=1000)), y,
+                       [3, 8, 12])
+    for _, _, fits in out:
+        for (support, weights, trace, iters), w in zip(fits, want):
+            np.testing.assert_array_equal(support, w.model.support)
+            assert iters == w.iterations
+            np.testing.assert_allclose(weights, w.model.weights, rtol=1e-12, atol=0)
+            np.testing.assert_allclose(trace, w.loss_trace, rtol=1e-12, atol=0)
+
+
+def _nccl_multi_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        import paper_1608_01398_b200 as gi
+        from paper_1608_01398_b200.dist import ShardedGenotypes, TorchComm
+        from paper_1608_01398_b200.simulate import SimulationSpec, simulate_phenotype
+
+        comm = TorchComm()
+        geno = ShardedGenotypes.synthetic(N, P, SEED, comm, device=rank, missing_rate=0.01)
+        view = gi.StandardizedView(geno, gi.CovariateBlock.build(None, n=N))
+        y, _ = simulate_phenotype(view, SimulationSpec(k_true=K, seed=5))
+        res = gi.fit(view, y, gi.IhtConfig(k=K))
+        q.put((rank, y, res.model.support, res.model.weights, res.loss_trace, res.iterations,
+               geno.native_comm().kind))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_two_or_more_gpus_match_single_device_fit():
+    """The production multi-GPU path: one process per GPU, NCCL communicator,
+    in-place device all-reduces and all-gathers across ranks.  Needs >= 2
+    GPUs (the round-end pool has one; skipped there, runs on any multi-GPU
+    node)."""
+    import torch
+
+    world = min(torch.cuda.device_count(), 8)
+    if world < 2:
+        pytest.skip(f"needs >= 2 GPUs for cross-GPU NCCL ranks (found {world})")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_multi_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    out = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p_ in procs:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    import paper_1608_01398_b200 as gi
+
+    y = out[0][1]
+    full = gi.PackedGenotypeMatrix.synthetic(N, P, SEED, missing_rate=0.01)
+    want = gi.fit(gi.StandardizedView(full, gi.CovariateBlock.build(None, n=N)), y,
+                  gi.IhtConfig(k=K))
+    for rank, _, support, weights, trace, iters, kind in out:
+        assert kind == "nccl"
+        np.testing.assert_array_equal(support, want.model.support)
+        assert iters == want.iterations
+        np.testing.assert_allclose(weights, want.model.weights, rtol=1e-9)
+        np.testing.assert_allclose(trace, want.loss_trace, rtol=1e-9)

@@ -116,3 +116,32 @@ def test_covariate_block():
     np.testing.assert_array_equal(block.values[:, 0], np.ones(10))
     assert block.labels[0] == "intercept"
     np.testing.assert_allclose(block.values[:, 1:].mean(axis=0), 0.0, atol=1e-12)
+
+
+def test_fit_path_runs_sharded_fits_one_at_a_time(monkeypatch):
+    """Sharded views share one communicator per process group, so fit_path
+    must not run their fits concurrently (advisor finding, round 1)."""
+    import numpy as np
+
+    from paper_1608_01398_b200 import model_select as ms
+
+    seen = {}
+
+    def fake_run(jobs, workers):
+        seen["workers"] = workers
+        return [(None, None) for _ in jobs]
+
+    class Shard:  # what dist.ShardedGenotypes looks like to fit_path
+        n, p = 10, 20
+        comm = object()
+
+        def native_comm(self):  # pragma: no cover - never called here
+            raise AssertionError
+
+    class View:
+        genotypes = Shard()
+        n, p, c = 10, 20, 0
+
+    monkeypatch.setattr(ms, "_run_concurrently", fake_run)
+    ms.fit_path(View(), np.zeros(10), [1, 2, 3], workers=8)
+    assert seen["workers"] == 1
