@@ -18,16 +18,26 @@ every X^T r streams from HBM (no flush needed).
   roofline  the X^T r kernel (aty_fast_kernel): algorithmic bytes per launch
           (p*ceil(n/4) + 8n + 24p) over its average
           CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline  the reference algorithm on the host (oracle/, C restatement of
-          genoiht's numba kernels, all host threads): one X^T r sweep over a
-          p-slice of the same matrix, extrapolated to full p; the reference
-          spends >97% of a config-3 fit in X^T r.
+  cpu_baseline  the reference's own CPU path on the host: genoiht 0.1.0 itself
+          (installed unmodified into baseline/_ref; its numba kernels on all
+          host threads) fitting the first ~0.4 GB of SNPs of the same matrix
+          with the same response law; per-iteration time is scaled by p / p_slice
+          (the reference spends >97% of a config-3 iteration in work linear in
+          p).  The oracle port stands in when baseline/_ref
+          is absent (kind "port").
+  parity  the timed fit against the oracle fit on the same bytes (support,
+          iterations, reason equal; beta / loss relative differences), N=1.
 
---impl reference runs only that CPU path (rank 0), one bounded p-slice sweep
-per step, extrapolated to the same metric.
+--impl reference runs only that CPU path (rank 0): one slice fit per step,
+ms_per_step = the wall time a step took, value scaled to the full matrix
+("extrapolated" states the factor).
 
-Multi-GPU: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N
-shards the SNPs over N ranks (NCCL); the fit size stays fixed (strong scaling).
+Multi-GPU: `bench.py --gpus N` launches N ranks itself through
+torch.distributed.run when WORLD_SIZE is unset (or run it under torchrun):
+one process per GPU, the SNPs sharded over the ranks, NCCL for the n-vector
+all-reduces and the top-k candidate all-gathers; the fit size stays fixed
+(strong scaling).  The timed loop runs uninstrumented; X^T r launch times
+come from a separate instrumented pass.
 """
 
 from __future__ import annotations
@@ -64,8 +74,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=1608)
     ap.add_argument("--pheno-seed", type=int, default=1398)
     ap.add_argument("--cpu-slice", type=int, default=0,
-                    help="SNPs in the CPU-baseline sample (0 = auto, ~2.5 GB)")
+                    help="SNPs in the CPU sample (0 = auto, ~0.4 GB of packed genotypes)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-parity", dest="parity", action="store_false",
+                    help="skip the parity leg (oracle fit on the same bytes, N=1 only)")
     ap.add_argument("--workload", default="c3", choices=["c3", "c2path", "c4cv", "c5"],
                     help="c3 (default, the metric's config), c2path (BASELINE config 2: "
                          "k=10..50 model-size path at n=5k x p=100k), c4cv (config 4: "
@@ -198,30 +210,92 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU leg
-def cpu_slice_sweep(n, p_slice, seed, missing, reps):
-    """Reference algorithm on the host: the oracle's C restatement of
-    _aty_kernel over a p-slice generated by the CPU twin of the generator.
-    Returns (best seconds per sweep, threads)."""
+def load_genoiht():
+    """The UNMODIFIED reference package, installed into baseline/_ref by
+    `pip install --no-index --no-deps --target baseline/_ref <reference pkg>`
+    (git-ignored; travels to the GPU box with the snapshot).  None when absent."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "genoiht")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/genoiht_numba_cache")
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    try:
+        import genoiht
+    except Exception as exc:  # numba missing or broken: fall back to the port
+        print(f"bench: reference package not importable ({exc}); timing the oracle port",
+              file=sys.stderr)
+        return None
+    return genoiht
+
+
+def slice_snps(n):
+    """SNPs of the CPU sample: ~0.4 GB of packed genotypes, so one reference
+    X^T r sweep takes ~0.1-0.3 s and a whole fit a few seconds."""
+    nb = (n + 3) // 4
+    return max(2000, int(0.4e9 // nb))
+
+
+def reference_slice_fits(n, p, p_slice, seed, missing, k, pheno_seed, reps):
+    """The reference's own CPU implementation of the path, timed: cold-start
+    IHT fits through genoiht's public API (genoiht.fit, reference iht.py:326 ->
+    _aty_kernel geno_matrix.py:142) on the first p_slice SNPs of the
+    workload's matrix (same bytes: the CPU twin of the device generator),
+    with all host threads.  The matrix is built with the SURVEY.md section
+    8(c) adapter (variant-major bytes + genoiht's own _packed_stats; data_t is
+    never read at these support sizes).  Falls back to the oracle port when
+    baseline/_ref is absent.  Returns a dict with per-fit seconds and
+    iterations, the thread count and the kind ("reference" | "port")."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle
+    import oracle  # the CPU twin of the synthetic-BED generator (same bytes)
 
     threads = os.cpu_count() or 1
-    oracle.set_threads(threads)
     data = oracle.synth_bed(seed, n, 0, p_slice, missing=missing)
-    u, v = oracle.stats(data, n)
-    mat = oracle.OraclePacked(n=n, p=p_slice, data=data, u=u, v=v)
-    r = np.random.default_rng(7).standard_normal(n)
-    times = []
+    genoiht = load_genoiht()
+    kk = min(k, p_slice)
+    if genoiht is not None:
+        from genoiht import geno_matrix as ref_gm
+
+        threads = genoiht.set_worker_threads(threads)
+        u, v = ref_gm._packed_stats(data, n)
+        mat = genoiht.PackedGenotypeMatrix(n=n, p=p_slice, data=data,
+                                           data_t=np.zeros((n, 0), np.uint8), u=u, v=v)
+        view = genoiht.StandardizedView(mat, genoiht.CovariateBlock.build(None, n=n))
+        y, _ = genoiht.simulate_phenotype(view, genoiht.SimulationSpec(k_true=kk, seed=pheno_seed))
+
+        def one():
+            return genoiht.fit(view, y, genoiht.IhtConfig(k=kk)).iterations
+        kind = "reference"
+        what = "genoiht 0.1.0 (baseline/_ref, numba) fit()"
+    else:
+        oracle.set_threads(threads)
+        mat = oracle.OraclePacked.from_bed(data, n)
+        view = oracle.OracleView(mat, oracle.intercept(n))
+        rng = np.random.default_rng(pheno_seed)
+        causal = np.sort(rng.choice(p_slice, size=kk, replace=False)).astype(np.int64)
+        eff = rng.normal(0.0, np.sqrt(0.01), size=kk)
+        y = mat.ax_columns(causal, eff) + rng.normal(0.0, np.sqrt(0.01), size=n)
+
+        def one():
+            return oracle.fit(view, y, kk).iterations
+        kind = "port"
+        what = "oracle port (C restatement of genoiht's kernels + its solver) fit"
+    secs, iters = [], []
     for _ in range(reps):
         t0 = time.perf_counter()
-        mat.aty_genetic(r)
-        times.append(time.perf_counter() - t0)
-    return times, threads
+        iters.append(one())
+        secs.append(time.perf_counter() - t0)
+    return {"secs": secs, "iters": iters, "threads": threads, "kind": kind, "what": what,
+            "k": kk}
 
 
-def auto_slice(n):
-    nb = (n + 3) // 4
-    return max(1000, int(2.5e9 // nb))
+def slice_rate(rec, p, p_slice, skip=0):
+    """it/s of the full-p workload from the slice fits: the reference spends
+    >97% of a config-3 iteration in work linear in p (X^T r, top-k, axpy;
+    SURVEY.md section 0), so per-iteration time is scaled by p / p_slice."""
+    secs, iters = rec["secs"][skip:], rec["iters"][skip:]
+    t_it = sum(secs) / max(sum(iters), 1)
+    return 1.0 / (t_it * p / p_slice), t_it
 
 
 def secondary_shape(workload):
@@ -299,24 +373,29 @@ def reference_arm(a):
     if a.workload in ("c2path", "c4cv"):
         reference_secondary(a)
         return
-    p_slice = min(a.p, a.cpu_slice or auto_slice(a.n))
-    times, threads = cpu_slice_sweep(a.n, p_slice, a.seed, a.missing, a.warmup + a.steps)
-    timed = times[a.warmup:]
-    t_iter = statistics.median(timed) * a.p / p_slice
-    value = 1.0 / t_iter
+    p_slice = min(a.p, a.cpu_slice or slice_snps(a.n))
+    rec = reference_slice_fits(a.n, a.p, p_slice, a.seed, a.missing, a.k, a.pheno_seed,
+                               a.warmup + a.steps)
+    value, t_it = slice_rate(rec, a.p, p_slice, skip=a.warmup)
+    timed = rec["secs"][a.warmup:]
     nb = (a.n + 3) // 4
-    sample = (f"oracle C restatement of genoiht _aty_kernel (one X^T r = one IHT iteration's "
-              f"dominant work) over n={a.n} x {p_slice} SNPs ({p_slice * nb / 1e9:.2f} GB), "
-              f"extrapolated x{a.p / p_slice:.1f} to p={a.p}; median of {len(timed)} steps")
+    sample = (f"{rec['what']} with k={rec['k']} on the first {p_slice} of the workload's "
+              f"{a.p} SNPs at n={a.n} ({p_slice * nb / 1e9:.2f} GB packed, same bytes), "
+              f"{rec['threads']} host threads; one fit per step; per-iteration time scaled "
+              f"by p / p_slice = {a.p / p_slice:.1f} to the full matrix")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "it/s",
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": 1e3 * t_iter, "higher_is_better": True, "scaling": "strong",
+            # the wall time a step actually took (one slice fit)
+            "ms_per_step": 1e3 * statistics.mean(timed),
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(a, a.gpus),  # the workload our arm runs at this N
-            "host": "reference algorithm on the box's host cores (no GPU)",
-            "xtr_packed_gbs": p_slice * nb / statistics.median(timed) / 1e9,
-            "cpu_baseline": {"value": value, "unit": "it/s", "cores": threads, "kind": "port",
-                             "sample": sample},
+            "host": "reference CPU path on the box's host cores (no GPU)",
+            "extrapolated": {"from_p": p_slice, "to_p": a.p, "factor": a.p / p_slice,
+                             "seconds_per_iteration_slice": t_it,
+                             "iterations_per_step": rec["iters"][a.warmup:]},
+            "cpu_baseline": {"value": value, "unit": "it/s", "cores": rec["threads"],
+                             "kind": rec["kind"], "sample": sample},
             "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -432,17 +511,82 @@ def secondary(a):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(a):
+    """`bench.py --gpus N` without a torchrun environment: launch the N ranks
+    ourselves (one process per GPU, NCCL) through torch.distributed.run on
+    127.0.0.1, with the same arguments; rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench: launching {a.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def rel_diff(a, b):
+    """max |a - b| / |b| over the entries (inf on a shape mismatch)."""
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        return float("inf")
+    if not a.size:
+        return 0.0
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+def parity_leg(matrix, y, k, got):
+    """The fit the timed loop ran, checked against the oracle (the reference
+    algorithm restated on the host and pinned to golden vectors the reference
+    produced, tests/test_oracle.py) on the same bytes and response: support,
+    iteration count and reason equal; beta, b_cov and the loss trace within
+    1e-6 relative (north star)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    t0 = time.perf_counter()
+    data = np.asarray(matrix.data)  # the verbatim BED bytes, read back from the device
+    ref = oracle.OraclePacked.from_bed(data, matrix.n)
+    stats_equal = bool(np.array_equal(ref.u, matrix.u) and np.array_equal(ref.v, matrix.v))
+    oracle.set_threads(os.cpu_count() or 1)
+    t1 = time.perf_counter()
+    want = oracle.fit(oracle.OracleView(ref, oracle.intercept(matrix.n)), y, k)
+    t2 = time.perf_counter()
+    out = {"checker": "oracle (C + numpy restatement of genoiht, pinned to its golden vectors)",
+           "support_equal": bool(np.array_equal(got.model.support, want.support)),
+           "iterations_equal": got.iterations == want.iterations,
+           "reason_equal": got.reason == want.reason,
+           "stats_bit_identical": stats_equal,
+           "beta_max_rel": rel_diff(got.model.weights, want.weights),
+           "covar_max_rel": rel_diff(got.model.covar, want.covar),
+           "loss_max_rel": rel_diff(got.loss_trace, want.loss_trace),
+           "iterations": [got.iterations, want.iterations],
+           "oracle_fit_s": t2 - t1, "readback_and_stats_s": t1 - t0}
+    out["ok"] = bool(out["support_equal"] and out["iterations_equal"] and out["reason_equal"]
+                     and out["beta_max_rel"] <= 1e-6 and out["loss_max_rel"] <= 1e-6)
+    del data
+    return out
+
+
 def main():
     a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if a.impl == "reference":
         reference_arm(a)
+        return
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(a))
+    if os.environ.get("GI_BENCH_PROBE_RANKS") == "1":  # tests: the rank launch alone
+        print(json.dumps({"probe_rank": int(os.environ.get("RANK", "0")), "world": world,
+                          "master_addr": os.environ.get("MASTER_ADDR")}), flush=True)
         return
     if a.workload not in ("c3", "c5"):
         secondary(a)
         return
     import torch
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # GI_DIST_BACKEND=gloo lets several ranks share one GPU (host-staged
@@ -453,6 +597,7 @@ def main():
     torch.cuda.set_device(local)
     import paper_1608_01398_b200 as gi
     from paper_1608_01398_b200 import dist as gdist
+    from paper_1608_01398_b200 import iht as giht
     from paper_1608_01398_b200.simulate import SimulationSpec, simulate_phenotype
 
     # GI_FORCE_SHARDED=1 runs the sharded path (its communicator and exchange
@@ -481,19 +626,22 @@ def main():
     cfg = gi.IhtConfig(k=a.k)
     stream = torch.cuda.current_stream()
 
-    # ---- device-resident fits (value)
-    from paper_1608_01398_b200 import iht as giht
-
-    counters = {}
-
     def run_fit():
         return gi.fit(view, y, cfg, _resident=True)
+
     gi.fit(view, y, cfg)  # primes the native loop's resident inputs (sharded or not)
+    nccl_info = None
+    if sharded:
+        nc = geno.native_comm()
+        nccl_info = {"backend": nc.kind, "nranks": comm.world}
+        if rank == 0:
+            print(f"bench: native communicator {nc.kind}, nranks={comm.world}", file=sys.stderr,
+                  flush=True)
+
+    # ---- device-resident fits (value): the timed loop is not instrumented
+    for _ in range(a.warmup):
+        run_fit()
     with ClockSampler(local) as clocks:
-        for _ in range(a.warmup):
-            run_fit()
-        torch.cuda.synchronize()
-        giht.profile_native(counters)
         iters = 0
         last = None
         barrier()
@@ -507,13 +655,24 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        giht.profile_native(None)
     ms = e0.elapsed_time(e1)
-    aty_ms = [counters["aty_ms"] / max(counters["aty_launches"], 1)]
-    launches = counters["kernel_launches"]
     if world > 1:
         ms = comm.allreduce_max(ms)
     value = iters / (ms / 1e3)
+
+    # ---- instrumented pass (not timed): X^T r launch durations by CUDA events
+    # on the fit's stream, and the kernel launches per fit (identical fits, so
+    # the timed loop launched steps x this many)
+    counters = {}
+    n_prof = max(1, min(a.steps, 4))
+    giht.profile_native(counters, time_xtr=True)
+    for _ in range(n_prof):
+        run_fit()
+    giht.profile_native(None)
+    aty_avg = counters["aty_ms"] / max(counters["aty_launches"], 1)
+    launches = int(round(counters["kernel_launches"] / n_prof * a.steps))
+    if world > 1:
+        aty_avg = comm.allreduce_max(aty_avg)  # the slowest shard's sweep
 
     # ---- end to end through the public API (host y in, FitResult out)
     y_pin = torch.as_tensor(y).pin_memory().numpy()
@@ -562,21 +721,25 @@ def main():
     fmt = "base-3" if base3 else "2-bit"
     x_bytes = p_local * ((n + 4) // 5) if base3 else p_local * nb
     alg_bytes = x_bytes + 8 * n + 24 * p_local
-    aty_avg = statistics.mean(aty_ms) if aty_ms else float("nan")
     achieved = alg_bytes / (aty_avg / 1e3) / 1e9
     peak, peak_kind = measured_peak()
     traffic = traffic_from_profile(n, p_local, fmt, a.missing)
 
+    parity = None
+    if world == 1 and not sharded and a.parity:
+        parity = parity_leg(geno, y, a.k, last)
+
     cpu = None
     if world == 1 and not a.no_cpu:
-        p_slice = min(a.p, a.cpu_slice or auto_slice(a.n))
-        times, threads = cpu_slice_sweep(n, p_slice, a.seed, a.missing, 2)
-        t_iter = min(times) * a.p / p_slice
-        cpu = {"value": 1.0 / t_iter, "unit": "it/s", "cores": threads, "kind": "port",
-               "sample": f"oracle C restatement of _aty_kernel over n={n} x {p_slice} SNPs "
-                         f"({p_slice * nb / 1e9:.2f} GB), best of 2, extrapolated to p={a.p} "
-                         f"(X^T r is >97% of a reference config-3 iteration)",
-               "xtr_packed_gbs": p_slice * nb / min(times) / 1e9}
+        p_slice = min(a.p, a.cpu_slice or slice_snps(a.n))
+        rec = reference_slice_fits(n, a.p, p_slice, a.seed, a.missing, a.k, a.pheno_seed, 3)
+        cpu_value, t_it = slice_rate(rec, a.p, p_slice, skip=1)  # the first fit JITs
+        cpu = {"value": cpu_value, "unit": "it/s", "cores": rec["threads"], "kind": rec["kind"],
+               "sample": f"{rec['what']} with k={rec['k']} on the first {p_slice} SNPs at "
+                         f"n={n} ({p_slice * nb / 1e9:.2f} GB, same bytes), 2 timed fits "
+                         f"after one warm-up, per-iteration time scaled by p / p_slice = "
+                         f"{a.p / p_slice:.1f}",
+               "seconds_per_iteration_slice": t_it}
 
     h2d = 8 * n + 8 * n * cov.c  # response + covariate block uploaded per fit
     line = {
@@ -590,25 +753,31 @@ def main():
         # smallest are below the noise, so not every one is recoverable)
         "planted_recovered": (f"{np.intersect1d(last.model.support, truth.support).size}"
                               f"/{truth.support.size}") if last is not None else None,
-        # BED-equivalent: 2-bit packed genotype bytes per second (above the HBM
-        # bandwidth when the kernel streams the 1.6-bit base-3 copy)
+        # BED-equivalent: 2-bit packed genotype bytes per second per GPU (above
+        # the HBM bandwidth when the kernel streams the 1.6-bit base-3 copy)
         "xtr_packed_gbs": p_local * nb / (aty_avg / 1e3) / 1e9,
+        "xtr_packed_gbs_all_gpus": a.p * nb / (aty_avg / 1e3) / 1e9,
         "xtr_ms": aty_avg,
         "xtr_format": ("base-3 device copy, 5 genotypes per byte (no missing genotypes)"
                        if base3 else "2-bit BED tiles"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "aty_fast_kernel", "bytes_per_launch": alg_bytes,
+                     "timing": f"CUDA events around each launch on the fit stream, "
+                               f"separate instrumented pass of {n_prof} fits",
                      "smem": smem_roofline(n, p_local, aty_avg, clk.get("sm_mhz"),
                                            torch.cuda.get_device_properties(local)
                                            .multi_processor_count, a.missing,
                                            miss_frac, base3)},
+        "parity": parity,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h // max(a.steps, 1)},
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if nccl_info is not None:
+        line["comm"] = nccl_info
     print(json.dumps(line), flush=True)
     if sharded:
         torch.distributed.destroy_process_group()

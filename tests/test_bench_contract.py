@@ -56,3 +56,21 @@ def test_reference_arm_under_torchrun_prints_once():
     assert res.returncode == 0, res.stderr
     (line,) = _lines(res.stdout)
     assert line["impl"] == "reference" and line["n_gpus"] == 2
+
+
+def test_gpus_flag_launches_the_ranks_itself():
+    """`python bench.py --gpus N` (the driver's form, no torchrun environment)
+    must start N ranks itself -- one process per GPU on 127.0.0.1 -- rather
+    than silently measuring one GPU.  GI_BENCH_PROBE_RANKS makes each rank
+    report its place in the world and exit before touching a GPU."""
+    env = _env()
+    env["GI_BENCH_PROBE_RANKS"] = "1"
+    for key in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(key, None)
+    res = subprocess.run([sys.executable, "bench.py", "--gpus", "3", "--steps", "1",
+                          "--warmup", "3"], cwd=ROOT, env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert res.returncode == 0, res.stderr
+    probes = sorted(_lines(res.stdout), key=lambda d: d["probe_rank"])
+    assert [d["probe_rank"] for d in probes] == [0, 1, 2]
+    assert all(d["world"] == 3 and d["master_addr"] == "127.0.0.1" for d in probes)
