@@ -210,6 +210,8 @@ typedef struct {
   double aty_ms_total;   /* out: summed X^T r kernel time (flags bit 0) */
   int64_t aty_launches;  /* out: X^T r launches */
   int reason;            /* out: 0 converged, 1 max-iter, 2 step-size collapse */
+  int xtr_kernel;        /* out: X^T r kernel the loop ran: 0 exact fp64, 1 fast over the
+                            2-bit tiles, 2 fast over the base-3 copy */
 } gi_fit_result;
 
 /* Replaces genoiht.fit (iht.py:326-354) on one GPU: the complete IHT loop with

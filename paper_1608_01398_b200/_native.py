@@ -47,7 +47,7 @@ class FitOut(ctypes.Structure):
                 ("covar", c_vp), ("loss_trace", c_vp), ("trace_cap", c_i64),
                 ("trace_len", c_i64), ("iterations", c_i64), ("backtracks", c_i64),
                 ("kernel_launches", c_i64), ("aty_ms_total", c_dbl), ("aty_launches", c_i64),
-                ("reason", c_int)]
+                ("reason", c_int), ("xtr_kernel", c_int)]
 
 
 def _declare(lib):

@@ -893,6 +893,7 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
             (long long)iterations, F.syncs, F.sync_us, F.launches,
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start)
                 .count());
+  res->xtr_kernel = F.exact_ ? 0 : (h->desc().x3 != nullptr ? 2 : 1);
   res->kernel_launches = F.launches;
   res->aty_ms_total = F.aty_ms;
   res->aty_launches = F.aty_launches;

@@ -1,0 +1,90 @@
+"""Parity of the native loop's FAST X^T r kernels against the reference.
+
+The golden fits and CV runs in tests/golden/large.npz (tools/make_golden.py,
+produced by genoiht 0.1.0 itself) are big enough that the native loop runs
+the lookup-table X^T r kernel, not the exact fp64 one (more than 2 MiB of
+tiles and n > 8 (k + c + 1); csrc/fit.cu NativeFit): over the 2-bit tiles
+with the missing-sum lookups when genotypes are missing (2-3%), over the
+base-3 copy otherwise.  The matrices are rebuilt on the device by the
+generator whose CPU twin made the reference's bytes (checked by SHA-256).
+
+Bar (north star): support, iteration count and reason identical; beta, b_cov
+and the loss trace within 1e-6 relative (vector reading: see
+test_gpu_fit.vec_atol); CV: k_best, the fold-mean MSE curve, the final
+model.  CV runs both ways the device holds training folds: compact device
+copies (GI_CV_COMPACT=1) and row masks over the resident matrix (=0).
+"""
+import numpy as np
+import pytest
+
+import golden_io
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-6
+LARGE = golden_io.load("large")
+FITS = sorted(k for k, v in LARGE.items() if v["kind"] == "fit")
+CVS = sorted(k for k, v in LARGE.items() if v["kind"] == "cv")
+
+
+def vec_atol(want):
+    want = np.asarray(want, dtype=np.float64)
+    return RTOL * float(np.max(np.abs(want))) if want.size else 0.0
+
+
+def _matrix(case):
+    import paper_1608_01398_b200 as gi
+
+    m = gi.PackedGenotypeMatrix.synthetic(case["n"], case["p"], case["seed"],
+                                          missing_rate=case["missing"])
+    assert golden_io.sha(m.data) == case["data_sha"], "device generator drifted from the twin"
+    return m
+
+
+@pytest.mark.parametrize("name", FITS)
+def test_large_fit_matches_reference(name):
+    import paper_1608_01398_b200 as gi
+    from paper_1608_01398_b200.iht import last_native_fit_info
+
+    case = LARGE[name]
+    m = _matrix(case)
+    raw = case["covar_raw"]
+    block = gi.CovariateBlock.build(raw if raw.size else None, n=case["n"])
+    res = gi.fit(gi.StandardizedView(m, block), case["y"], gi.IhtConfig(k=int(case["k"])))
+    info = last_native_fit_info()
+    want_kernel = "fast-2bit" if case["missing"] > 0 else "fast-base3"
+    assert info["xtr_kernel"] == want_kernel, info
+    np.testing.assert_array_equal(res.model.support, case["support"])
+    assert res.iterations == case["iterations"] and res.reason == case["reason"]
+    np.testing.assert_allclose(res.model.weights, case["weights"], rtol=RTOL,
+                               atol=vec_atol(case["weights"]))
+    np.testing.assert_allclose(res.model.covar, case["covar"], rtol=RTOL,
+                               atol=vec_atol(case["covar"]) + 1e-12)
+    np.testing.assert_allclose(res.loss_trace, case["loss_trace"], rtol=RTOL, atol=1e-12)
+
+
+@pytest.mark.parametrize("compact", ["1", "0"], ids=["compact-folds", "masked-folds"])
+@pytest.mark.parametrize("name", CVS)
+def test_large_cv_matches_reference(name, compact, monkeypatch):
+    import paper_1608_01398_b200 as gi
+    from paper_1608_01398_b200.iht import _xtr_exact
+
+    monkeypatch.setenv("GI_CV_COMPACT", compact)
+    case = LARGE[name]
+    m = _matrix(case)
+    # every fold fit is big enough for the fast kernel
+    n_train = case["n"] - np.bincount(case["labels"]).max()
+    assert not _xtr_exact(int(n_train), case["p"], int(case["path"].max()), 1)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=case["n"]))
+    plan = gi.CvPlan.build(case["n"], case["q"], case["path"], seed=case["fold_seed"])
+    np.testing.assert_array_equal(plan.fold_labels, case["labels"])
+    rep = gi.cv_iht(view, case["y"], plan, gi.IhtConfig(k=int(case["path"].max())),
+                    std_mode=case["std_mode"], warm_start=bool(case["warm"]))
+    assert rep.k_best == case["k_best"]
+    np.testing.assert_allclose(rep.mse, case["mse"], rtol=RTOL)
+    np.testing.assert_allclose(rep.mean_mse, case["mean_mse"], rtol=RTOL)
+    np.testing.assert_array_equal(rep.final_model.support, case["final_support"])
+    np.testing.assert_allclose(rep.final_model.weights, case["final_weights"], rtol=RTOL,
+                               atol=vec_atol(case["final_weights"]))
+    np.testing.assert_allclose(rep.final_model.covar, case["final_covar"], rtol=RTOL,
+                               atol=1e-12)

@@ -86,3 +86,41 @@ def test_synth_twin_distribution():
     # slices are independent of how the SNP range is cut
     np.testing.assert_array_equal(oracle.synth_bed(1608, 4000, 100, 50, missing=0.02),
                                   data[100:150])
+
+
+LARGE = golden_io.load("large")
+
+
+def _large_matrix(case):
+    data = oracle.synth_bed(case["seed"], case["n"], 0, case["p"], missing=case["missing"])
+    assert golden_io.sha(data) == case["data_sha"], "synthetic-BED twin drifted"
+    return oracle.OraclePacked.from_bed(data, case["n"])
+
+
+@pytest.mark.parametrize("name", sorted(k for k, v in LARGE.items() if v["kind"] == "fit"))
+def test_oracle_large_fit_matches_reference(name):
+    """The fast-kernel-sized golden fits (tests/test_gpu_large_parity.py):
+    the oracle reproduces the reference on them, so the GPU comparison is
+    against pinned numbers."""
+    from paper_1608_01398_b200.geno_matrix import CovariateBlock
+
+    case = LARGE[name]
+    m = _large_matrix(case)
+    raw = case["covar_raw"]
+    cov = CovariateBlock.build(raw if raw.size else None, n=case["n"]).values
+    res = oracle.fit(oracle.OracleView(m, cov), case["y"], int(case["k"]))
+    np.testing.assert_array_equal(res.support, case["support"])
+    assert res.iterations == case["iterations"] and res.reason == case["reason"]
+    np.testing.assert_allclose(res.weights, case["weights"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(res.loss_trace, case["loss_trace"], rtol=1e-12, atol=1e-15)
+
+
+def test_oracle_large_cv_matches_reference():
+    case = LARGE["cvL_global_warm_miss"]
+    m = _large_matrix(case)
+    rep = oracle.cv(oracle.OracleView(m, oracle.intercept(case["n"])), case["y"], case["q"],
+                    case["path"], case["fold_seed"], std_mode=case["std_mode"],
+                    warm_start=bool(case["warm"]))
+    assert rep.k_best == case["k_best"]
+    np.testing.assert_allclose(rep.mse, case["mse"], rtol=1e-10, atol=1e-14)
+    np.testing.assert_array_equal(rep.final[0], case["final_support"])

@@ -148,9 +148,81 @@ def cv_cases():
     return cases
 
 
+def _synth_matrix(n, p, seed, missing):
+    """The device generator's bytes (its CPU twin in oracle/), as a reference
+    matrix: the GPU tests rebuild the same matrix with
+    PackedGenotypeMatrix.synthetic(n, p, seed, missing_rate=missing)."""
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "oracle"))
+    import oracle
+    data = oracle.synth_bed(seed, n, 0, p, missing=missing)
+    return PackedGenotypeMatrix.from_bed_buffer(data, n)
+
+
+def large_cases():
+    """Fits and CV runs big enough for the native loop's FAST X^T r kernel
+    (> 2 MiB of tiles and n > 8 (k + c + 1): csrc/fit.cu NativeFit), with and
+    without missing genotypes (2-bit tiles with the missing-sum lookups, or
+    the base-3 copy), covariates, warm starts and both CV standardisations."""
+    cases = []
+    fit_specs = [
+        dict(name="fit_miss3", n=4000, p=20000, seed=4242, missing=0.03, k_true=12,
+             pheno_seed=11, ks=[6, 12, 25], ncov=0),
+        dict(name="fit_miss2_cov", n=4100, p=16000, seed=4343, missing=0.02, k_true=10,
+             pheno_seed=12, ks=[10, 18], ncov=2),
+        dict(name="fit_base3_cov", n=3333, p=24000, seed=4444, missing=0.0, k_true=15,
+             pheno_seed=13, ks=[15], ncov=1),
+    ]
+    for sp in fit_specs:
+        m = _synth_matrix(sp["n"], sp["p"], sp["seed"], sp["missing"])
+        raw = None
+        if sp["ncov"]:
+            raw = np.random.default_rng(sp["seed"] + 7).standard_normal((sp["n"], sp["ncov"]))
+        view = StandardizedView(m, CovariateBlock.build(raw, n=sp["n"]))
+        y, truth = simulate_phenotype(view, SimulationSpec(k_true=sp["k_true"],
+                                                           seed=sp["pheno_seed"]))
+        for k in sp["ks"]:
+            res = fit(view, y, IhtConfig(k=k))
+            cases.append(dict(
+                kind="fit", name=f"{sp['name']}_k{k}", n=sp["n"], p=sp["p"], seed=sp["seed"],
+                missing=sp["missing"], k=k, covar_raw=raw if raw is not None else np.zeros(0),
+                data_sha=sha(m.data), y=y, truth=truth.support, support=res.model.support,
+                weights=res.model.weights, covar=res.model.covar, loss_trace=res.loss_trace,
+                iterations=res.iterations, reason=res.reason))
+    cv_specs = [
+        dict(name="cvL_train_cold", n=3000, p=12000, seed=5151, missing=0.0, q=5,
+             path=np.arange(1, 9), fold_seed=2016, std_mode="train", warm=False),
+        dict(name="cvL_global_cold", n=3000, p=12000, seed=5151, missing=0.0, q=5,
+             path=np.arange(1, 9), fold_seed=2016, std_mode="global", warm=False),
+        dict(name="cvL_train_warm_miss", n=2600, p=14000, seed=5252, missing=0.02, q=4,
+             path=np.arange(2, 12, 2), fold_seed=77, std_mode="train", warm=True),
+        dict(name="cvL_global_warm_miss", n=2600, p=14000, seed=5252, missing=0.02, q=4,
+             path=np.arange(2, 12, 2), fold_seed=77, std_mode="global", warm=True),
+    ]
+    for sp in cv_specs:
+        m = _synth_matrix(sp["n"], sp["p"], sp["seed"], sp["missing"])
+        view = StandardizedView(m, CovariateBlock.build(None, n=sp["n"]))
+        y, truth = simulate_phenotype(view, SimulationSpec(k_true=6, seed=sp["seed"] + 1))
+        plan = CvPlan.build(sp["n"], sp["q"], sp["path"], seed=sp["fold_seed"])
+        rep = cv_iht(view, y, plan, IhtConfig(k=int(sp["path"].max())), std_mode=sp["std_mode"],
+                     warm_start=sp["warm"])
+        cases.append(dict(
+            kind="cv", name=sp["name"], n=sp["n"], p=sp["p"], seed=sp["seed"],
+            missing=sp["missing"], q=sp["q"], path=sp["path"], fold_seed=sp["fold_seed"],
+            std_mode=sp["std_mode"], warm=sp["warm"], data_sha=sha(m.data), y=y,
+            labels=plan.fold_labels, mse=rep.mse, mean_mse=rep.mean_mse, k_best=rep.k_best,
+            final_support=rep.final_model.support, final_weights=rep.final_model.weights,
+            final_covar=rep.final_model.covar))
+    return cases
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
-    for group, fn in [("kernels", kernel_cases), ("fits", fit_cases), ("cv", cv_cases)]:
+    groups = [("kernels", kernel_cases), ("fits", fit_cases), ("cv", cv_cases),
+              ("large", large_cases)]
+    only = sys.argv[1:]
+    for group, fn in groups:
+        if only and group not in only:
+            continue
         cases = fn()
         payload = {}
         for c in cases:
