@@ -96,7 +96,10 @@ int gi_matrix_masked_stats(const gi_matrix *h, const uint8_t *keep, double *u, d
 /* ------------------------------------------------ operator protocol (host) */
 /* aty_genetic (geno_matrix.py:351-364).  mode 0: exact -- bit-identical to
  * _aty_kernel (:142-165) when sum_r is numpy's r.sum(); mode 1: fast lookup-
- * table kernel (fp32 tables, fp64 accumulation; sum_r ignored). */
+ * table kernel (fp32 tables, fp64 accumulation; sum_r ignored); mode 2:
+ * tensor-core kernel (tcgen05.mma kind::i8 over the 2-bit tiles: exact
+ * integer sums of the residual quantised to 2^-26 of its range; sum_r
+ * ignored). */
 int gi_aty(gi_matrix *h, const double *r, double sum_r, double *out, int mode);
 /* Batched aty_genetic for B right-hand sides, e.g. the residuals of q CV folds
  * (zero outside each fold) with each fold's own statistics (reference
@@ -104,9 +107,11 @@ int gi_aty(gi_matrix *h, const double *r, double sum_r, double *out, int mode);
  * R is (B, n) row-major; U, V are (B, p) row-major per-RHS stats, or NULL for
  * the handle's; sum_R[b] plays sum_r of gi_aty (mode 0; may be NULL in mode 1);
  * G is (B, p).  G[b] equals gi_aty of R[b] under stats (U[b], V[b]) -- bit for
- * bit in mode 0.  One X^T r sweep per RHS, queued back to back on the matrix's
- * stream with one host sync (a fused multi-RHS sweep does not pay on B200:
- * DESIGN.md section 9). */
+ * bit in mode 0.  Modes 0 and 1: one X^T r sweep per RHS, queued back to back
+ * on the matrix's stream with one host sync.  Mode 2 (the multi-RHS X^T R):
+ * ONE tensor-core sweep of the tiles per batch of up to 32 right-hand sides
+ * (16 when the matrix has missing genotypes); each decoded genotype tile feeds
+ * every right-hand side of the batch (xtr_mma.cu). */
 int gi_aty_batched(gi_matrix *h, const double *R, const double *sum_R, const double *U,
                    const double *V, int64_t B, double *G, int mode);
 /* ax_columns (geno_matrix.py:328-349), bit-identical to _ax_cols_kernel (:168-194) */

@@ -380,12 +380,81 @@ static int aty_enqueue(gi_matrix* h, const double* r, double sum_r, const double
   return 0;
 }
 
+// Whether the matrix holds any missing genotype (cached on the handle).
+static int has_missing(gi_matrix* h, bool& out) {
+  if (h->any_missing < 0) {
+    std::vector<uint8_t> flags((size_t)h->G);
+    if (h->G)
+      GI_CUDA_TRY(cudaMemcpy(flags.data(), h->gmiss->ptr, (size_t)h->G, cudaMemcpyDeviceToHost));
+    int any = 0;
+    for (uint8_t f : flags) any |= f ? 1 : 0;
+    h->any_missing = any;
+  }
+  out = h->any_missing != 0;
+  return 0;
+}
+
+// Tensor-core X^T R (xtr_mma.cu) for B residuals (rows of R, host), optional
+// per-RHS stats U, V (rows, host): batches of up to 32 residuals (16 when the
+// matrix has missing genotypes) per sweep of the tiles.
+static int aty_mma_enqueue(gi_matrix* h, const double* R, const double* U, const double* V,
+                           int64_t B, double* G) {
+  bool miss = false;
+  TRY(has_missing(h, miss));
+  const int64_t maxb = miss ? 16 : 32, n = h->n, p = h->p;
+  const gi::MatrixDesc d = h->desc();
+  const int64_t bsz = std::min<int64_t>(maxb, B);
+  const int64_t qbytes = gi::xtr_mma_qimg_bytes(d, (int)bsz);
+  const int64_t pcap = 4 * 148 * bsz;
+  // s_e: R (bsz x n) | qscal (2 bsz) | qsum (bsz) | partials | tickets | digit image
+  const size_t off_q = ((sizeof(double) * (size_t)(bsz * n + 3 * bsz + pcap) +
+                         sizeof(unsigned int) * (size_t)bsz) + 1023) & ~(size_t)1023;
+  TRY(h->s_e.ensure(off_q + (size_t)qbytes, h->device));
+  TRY(h->s_b.ensure(sizeof(double) * (size_t)(bsz * p), h->device));
+  double* dR = h->s_e.as<double>();
+  double* qscal = dR + bsz * n;
+  long long* qsum = reinterpret_cast<long long*>(qscal + 2 * bsz);
+  double* partials = reinterpret_cast<double*>(qsum + bsz);
+  unsigned int* tickets = reinterpret_cast<unsigned int*>(partials + pcap);
+  int8_t* qimg = reinterpret_cast<int8_t*>(h->s_e.as<char>() + off_q);
+  double *du = h->du(), *dv = h->dv();
+  if (U) {
+    TRY(h->s_d.ensure(sizeof(double) * 2 * (size_t)(bsz * p), h->device));
+    du = h->s_d.as<double>();
+    dv = du + bsz * p;
+  }
+  GI_CUDA_TRY(cudaMemsetAsync(tickets, 0, sizeof(unsigned int) * bsz, h->stream));
+  for (int64_t b0 = 0; b0 < B; b0 += bsz) {
+    const int64_t nb = std::min<int64_t>(bsz, B - b0);
+    GI_CUDA_TRY(cudaMemcpyAsync(dR, R + b0 * n, sizeof(double) * nb * n, cudaMemcpyHostToDevice,
+                                h->stream));
+    if (U) {
+      GI_CUDA_TRY(cudaMemcpyAsync(du, U + b0 * p, sizeof(double) * nb * p,
+                                  cudaMemcpyHostToDevice, h->stream));
+      GI_CUDA_TRY(cudaMemcpyAsync(dv, V + b0 * p, sizeof(double) * nb * p,
+                                  cudaMemcpyHostToDevice, h->stream));
+    }
+    TRY(gi::launch_xtr_quant(n, h->T, (int)nb, dR, n, nullptr, 0, qscal, qsum, qimg, partials,
+                             pcap, tickets, h->stream));
+    TRY(gi::launch_xtr_mma(d, static_cast<const uint8_t*>(h->gmiss->ptr), miss, (int)nb, qimg,
+                           qscal, qsum, du, dv, static_cast<const int32_t*>(h->s1cnt->ptr),
+                           U ? p : 0, 0, 1.0, h->s_b.as<double>(), p, nullptr, h->sms,
+                           h->stream));
+    GI_CUDA_TRY(cudaMemcpyAsync(G + b0 * p, h->s_b.mem->ptr, sizeof(double) * nb * p,
+                                cudaMemcpyDeviceToHost, h->stream));
+  }
+  return 0;
+}
+
 int gi_aty(gi_matrix* h, const double* r, double sum_r, double* out, int mode) {
   CHECK_ARG(h && r && out, "NULL argument");
   if (h->p == 0) return 0;
   std::lock_guard<std::mutex> lock(h->mu);
   DeviceGuard g(h->device);
-  TRY(aty_enqueue(h, r, sum_r, h->du(), h->dv(), out, mode));
+  if (mode == 2)
+    TRY(aty_mma_enqueue(h, r, nullptr, nullptr, 1, out));
+  else
+    TRY(aty_enqueue(h, r, sum_r, h->du(), h->dv(), out, mode));
   GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }
@@ -400,6 +469,11 @@ int gi_aty_batched(gi_matrix* h, const double* R, const double* sum_R, const dou
   std::lock_guard<std::mutex> lock(h->mu);
   DeviceGuard g(h->device);
   const int64_t p = h->p;
+  if (mode == 2) {
+    TRY(aty_mma_enqueue(h, R, U, V, B, G));
+    GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return 0;
+  }
   double *du = h->du(), *dv = h->dv();
   if (U) {
     TRY(h->s_d.ensure(sizeof(double) * 2 * p, h->device));

@@ -214,4 +214,18 @@ int launch_ax_residual(const MatrixDesc& m, const double* u, const double* v,
                        unsigned int* ticket, cudaStream_t s);
 int launch_decompress(const MatrixDesc& m, const double* u, const double* v,
                       const int64_t* idx, int64_t k, double* out_t, cudaStream_t s);
+// X^T R on the tensor cores (xtr_mma.cu): the digit image of up to 32
+// residuals (16 with missing genotypes), then one sweep of the 2-bit tiles
+int xtr_mma_cols(int nrhs);
+int64_t xtr_mma_qimg_bytes(const MatrixDesc& m, int nrhs);
+int launch_xtr_quant(int64_t n, int64_t T, int nrhs, const double* r, int64_t rstride,
+                     const uint8_t* keep, int64_t kstride, double* qscal, long long* qsum,
+                     int8_t* qimg, double* partials, int64_t partial_cap,
+                     unsigned int* tickets, cudaStream_t s);
+int launch_xtr_mma(const MatrixDesc& m, const uint8_t* gmiss, bool any_missing, int nrhs,
+                   const int8_t* qimg, const double* qscal, const long long* qsum,
+                   const double* u, const double* v, const int32_t* s1cnt, int64_t stat_stride,
+                   int64_t cnt_stride, double scale_out, double* out, int64_t out_stride,
+                   double* gmax, int num_sms, cudaStream_t s, const PubArgs* pub = nullptr,
+                   unsigned int* pub_ticket = nullptr, void* pub_out = nullptr);
 }  // namespace gi

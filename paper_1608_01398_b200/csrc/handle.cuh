@@ -138,7 +138,8 @@ struct gi_matrix {
   std::shared_ptr<DevMem> u, v;      // fp64[p], owned per handle
   cudaStream_t stream = nullptr;
   std::mutex mu;
-  Scratch s_a, s_b, s_c, s_d;
+  Scratch s_a, s_b, s_c, s_d, s_e;
+  int any_missing = -1;              // cached: any genotype code 01 (-1: not known yet)
   // Identity of this handle.  The native fit loop's workspaces (fit.cu) live
   // in a process-wide pool per device keyed by shape, so fits on any matrix of
   // that shape (CV fold copies, with_stats copies) reuse them; the uid tells

@@ -64,6 +64,16 @@ def unpack_codes(packed: np.ndarray, length: int) -> np.ndarray:
     return np.ascontiguousarray(out[:, :length])
 
 
+_ATY_MODES = {"exact": 0, "fast": 1, "mma": 2}
+
+
+def _aty_mode(mode: str) -> int:
+    try:
+        return _ATY_MODES[mode]
+    except KeyError:
+        raise ValueError(f"unknown X^T r mode {mode!r} (exact, fast or mma)") from None
+
+
 class _Handle:
     """Owns one gi_matrix*; freed when the last Python reference goes away."""
 
@@ -285,7 +295,8 @@ class PackedGenotypeMatrix:
         """Standardized X^T r over every column (reference :351-364).
 
         mode="exact" reproduces _aty_kernel bit-for-bit; mode="fast" is the
-        lookup-table kernel the IHT loop uses (relative error ~1e-7)."""
+        lookup-table kernel (relative error ~1e-7); mode="mma" the tensor-core
+        kernel over exact integer sums of the quantised residual (~1e-8)."""
         r = np.ascontiguousarray(r, dtype=np.float64)
         if r.shape != (self.n,):
             raise ValueError(f"residual vector must have length {self.n}")
@@ -295,15 +306,16 @@ class PackedGenotypeMatrix:
         if self.n == 0:
             out[:] = 0.0
             return out
-        check(lib().gi_aty(self._h.raw, ptr(r), float(r.sum()), ptr(out),
-                           0 if mode == "exact" else 1))
+        check(lib().gi_aty(self._h.raw, ptr(r), float(r.sum()), ptr(out), _aty_mode(mode)))
         return out
 
     def aty_batched(self, R, U=None, V=None, mode: str = "exact") -> np.ndarray:
         """aty_genetic for each row of R (B, n) -- e.g. CV fold residuals, zero
         off the fold -- optionally under per-row stats U, V (B, p); returns
         (B, p).  Row b equals aty_genetic(R[b]) on with_stats(U[b], V[b]),
-        bit for bit in exact mode.  One device call (gi_aty_batched)."""
+        bit for bit in exact mode.  One device call (gi_aty_batched); in
+        mode="mma" every batch of up to 32 residuals (16 when genotypes are
+        missing) is ONE sweep of the matrix on the tensor cores."""
         R = np.ascontiguousarray(np.atleast_2d(R), dtype=np.float64)
         if R.ndim != 2 or R.shape[1] != self.n:
             raise ValueError(f"residual matrix must have {self.n} columns")
@@ -321,7 +333,7 @@ class PackedGenotypeMatrix:
         sums = np.array([float(r.sum()) for r in R])
         check(lib().gi_aty_batched(self._h.raw, ptr(R), ptr(sums),
                                    None if U is None else ptr(U), None if V is None else ptr(V),
-                                   B, ptr(out), 0 if mode == "exact" else 1))
+                                   B, ptr(out), _aty_mode(mode)))
         return out
 
     def decompress(self, idx) -> np.ndarray:
