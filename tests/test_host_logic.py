@@ -145,3 +145,60 @@ def test_fit_path_runs_sharded_fits_one_at_a_time(monkeypatch):
     monkeypatch.setattr(ms, "_run_concurrently", fake_run)
     ms.fit_path(View(), np.zeros(10), [1, 2, 3], workers=8)
     assert seen["workers"] == 1
+
+
+def test_integration_install_dispatches_reference_entry_points(monkeypatch):
+    """paper_1608_01398_b200.integration.install(genoiht): the reference's fit
+    and cv_iht -- in every module that bound them -- go to the device loop for
+    device-resident views and stay the reference's otherwise; uninstall
+    restores them (host-side check with a stand-in device matrix)."""
+    import os
+    import sys
+
+    import numpy as np
+    import pytest
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ref = os.path.join(root, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "genoiht")):
+        pytest.skip("baseline/_ref not installed")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/genoiht_numba_cache")
+    sys.path.insert(0, ref)
+    try:
+        import genoiht
+        import genoiht.cli
+        import genoiht.model_select
+        from paper_1608_01398_b200 import iht as dev_iht
+        from paper_1608_01398_b200 import integration
+        from paper_1608_01398_b200 import model_select as dev_ms
+
+        calls = []
+        monkeypatch.setattr(dev_iht, "fit", lambda *a, **k: calls.append("fit") or "device-fit")
+        monkeypatch.setattr(dev_ms, "cv_iht", lambda *a, **k: calls.append("cv") or "device-cv")
+
+        class DeviceLike:
+            is_cuda = True
+            n, p = 4, 3
+
+        ref_fit = genoiht.iht.fit
+        view = genoiht.StandardizedView(DeviceLike(), None)
+        integration.install(genoiht)
+        integration.install(genoiht)  # idempotent
+        try:
+            assert genoiht.fit(view, np.zeros(4), genoiht.IhtConfig(k=1)) == "device-fit"
+            assert genoiht.model_select.fit(view, np.zeros(4), genoiht.IhtConfig(k=1)) == \
+                "device-fit"
+            assert genoiht.cli.fit is genoiht.fit
+            assert genoiht.cv_iht(view, np.zeros(4), None, None) == "device-cv"
+            assert calls == ["fit", "fit", "cv"]
+            # host views still take the reference path
+            codes = np.array([[0, 2, 3], [2, 3, 0], [3, 0, 2], [0, 0, 3]], np.uint8)
+            host = genoiht.StandardizedView(genoiht.PackedGenotypeMatrix.from_codes(codes), None)
+            res = genoiht.fit(host, np.array([1.0, -1.0, 0.5, 0.0]), genoiht.IhtConfig(k=1))
+            assert type(res).__module__ == "genoiht.iht"
+        finally:
+            integration.uninstall(genoiht)
+        assert genoiht.iht.fit is ref_fit and genoiht.fit is ref_fit
+        assert genoiht.model_select.fit is ref_fit
+    finally:
+        sys.path.remove(ref)
