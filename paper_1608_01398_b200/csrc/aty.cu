@@ -782,6 +782,63 @@ __global__ void __launch_bounds__(kExactWarps * 32) aty_exact_kernel(
   }
 }
 
+// Exact gradient on the support (after a fast sweep): one warp per listed
+// column, fp64 sums of dose * r and missing * r over the column (lane-strided,
+// then a fixed xor tree), g_j = scale * v_j (t_j - u_j (sum_r - m_j)) as
+// _aty_kernel forms it (geno_matrix.py:165).  The step size of the next
+// iteration, mu = ||g_S||^2 / ||X_S g_S||^2 (iht.py:233-244), depends on
+// these entries ALONE, and right after a converged warm start they are at the
+// level of the previous fit's tolerance (~1e-7 of rms(g)): the lookup-table
+// kernel's ~6e-7 rms(g) error would set their direction, and a backtracking
+// test within 1% of its threshold could flip (tools/cv_diag.py).  The fp64
+// sums here are accurate to ~1e-16 of the column's |terms|.
+__global__ void support_grad_kernel(MatrixDesc m, const double* __restrict__ r_pad,
+                                    const double* __restrict__ u, const double* __restrict__ v,
+                                    const double* __restrict__ sum_r, double scale,
+                                    const int64_t* __restrict__ idx, int64_t k,
+                                    double* __restrict__ out, double* __restrict__ pub_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t_idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t_idx >= k) return;
+  const int64_t j = idx[t_idx];
+  double t = 0.0, mm = 0.0;
+  const int64_t words = m.T * GI_TILE_WORDS;
+  for (int64_t wg = lane; wg < words; wg += 32) {
+    const int64_t tile = wg >> 5;
+    const int w = (int)(wg & 31);
+    const uint32_t wd = __ldg(reinterpret_cast<const uint32_t*>(m.x + word_offset(tile, j, w, m.G)));
+    const double* rr = r_pad + tile * GI_TILE_SAMPLES + 16 * w;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t code = (wd >> (2 * i)) & 3u;
+      const double ri = rr[i];
+      t += code == 2u ? ri : (code == 3u ? 2.0 * ri : 0.0);
+      mm += code == 1u ? ri : 0.0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t += __shfl_xor_sync(0xffffffffu, t, o);
+    mm += __shfl_xor_sync(0xffffffffu, mm, o);
+  }
+  if (lane == 0) {
+    const double g = scale * (v[j] * (t - u[j] * (*sum_r - mm)));
+    out[j] = g;
+    if (pub_out) pub_out[t_idx] = g;
+  }
+}
+
+int launch_support_grad(const MatrixDesc& m, const double* r_pad, const double* u,
+                        const double* v, const double* d_sum_r, double scale, const int64_t* idx,
+                        int64_t k, double* out, double* pub_out, cudaStream_t s) {
+  if (k <= 0 || m.p == 0) return 0;
+  const int warps = 4;
+  support_grad_kernel<<<(unsigned)((k + warps - 1) / warps), warps * 32, 0, s>>>(
+      m, r_pad, u, v, d_sum_r, scale, idx, k, out, pub_out);
+  GI_LAUNCH_CHECK();
+  return 0;
+}
+
 int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u, const double* v,
                      const double* d_sum_r, double scale, double* out, cudaStream_t s,
                      double* d_gmax, const PubArgs* pub, unsigned int* pub_ticket,

@@ -401,14 +401,15 @@ static int aty_mma_enqueue(gi_matrix* h, const double* R, const double* U, const
                            int64_t B, double* G) {
   bool miss = false;
   TRY(has_missing(h, miss));
-  const int64_t maxb = miss ? 16 : 32, n = h->n, p = h->p;
+  const int64_t maxb = gi::xtr_mma_max_rhs(miss), n = h->n, p = h->p;
   const gi::MatrixDesc d = h->desc();
   const int64_t bsz = std::min<int64_t>(maxb, B);
   const int64_t qbytes = gi::xtr_mma_qimg_bytes(d, (int)bsz);
   const int64_t pcap = 4 * 148 * bsz;
-  // s_e: R (bsz x n) | qscal (2 bsz) | qsum (bsz) | partials | tickets | digit image
-  const size_t off_q = ((sizeof(double) * (size_t)(bsz * n + 3 * bsz + pcap) +
-                         sizeof(unsigned int) * (size_t)bsz) + 1023) & ~(size_t)1023;
+  // s_e: R (bsz x n) | qscal (2 bsz) | qsum (bsz) | partials | tickets | descriptors | image
+  const size_t off_desc = ((sizeof(double) * (size_t)(bsz * n + 3 * bsz + pcap) +
+                            sizeof(unsigned int) * (size_t)bsz) + 255) & ~(size_t)255;
+  const size_t off_q = (off_desc + sizeof(gi::XtrRhs) * (size_t)bsz + 1023) & ~(size_t)1023;
   TRY(h->s_e.ensure(off_q + (size_t)qbytes, h->device));
   TRY(h->s_b.ensure(sizeof(double) * (size_t)(bsz * p), h->device));
   double* dR = h->s_e.as<double>();
@@ -416,6 +417,7 @@ static int aty_mma_enqueue(gi_matrix* h, const double* R, const double* U, const
   long long* qsum = reinterpret_cast<long long*>(qscal + 2 * bsz);
   double* partials = reinterpret_cast<double*>(qsum + bsz);
   unsigned int* tickets = reinterpret_cast<unsigned int*>(partials + pcap);
+  gi::XtrRhs* ddesc = reinterpret_cast<gi::XtrRhs*>(h->s_e.as<char>() + off_desc);
   int8_t* qimg = reinterpret_cast<int8_t*>(h->s_e.as<char>() + off_q);
   double *du = h->du(), *dv = h->dv();
   if (U) {
@@ -423,6 +425,19 @@ static int aty_mma_enqueue(gi_matrix* h, const double* R, const double* U, const
     du = h->s_d.as<double>();
     dv = du + bsz * p;
   }
+  std::vector<gi::XtrRhs> desc((size_t)bsz);
+  for (int64_t b = 0; b < bsz; ++b) {
+    gi::XtrRhs& x = desc[(size_t)b];
+    x.r = dR + b * n;
+    x.keep = nullptr;
+    x.u = U ? du + b * p : du;
+    x.v = U ? dv + b * p : dv;
+    x.s1cnt = static_cast<const int32_t*>(h->s1cnt->ptr);
+    x.out = h->s_b.as<double>() + b * p;
+    x.gmax = nullptr;
+  }
+  GI_CUDA_TRY(cudaMemcpyAsync(ddesc, desc.data(), sizeof(gi::XtrRhs) * desc.size(),
+                              cudaMemcpyHostToDevice, h->stream));
   GI_CUDA_TRY(cudaMemsetAsync(tickets, 0, sizeof(unsigned int) * bsz, h->stream));
   for (int64_t b0 = 0; b0 < B; b0 += bsz) {
     const int64_t nb = std::min<int64_t>(bsz, B - b0);
@@ -434,12 +449,10 @@ static int aty_mma_enqueue(gi_matrix* h, const double* R, const double* U, const
       GI_CUDA_TRY(cudaMemcpyAsync(dv, V + b0 * p, sizeof(double) * nb * p,
                                   cudaMemcpyHostToDevice, h->stream));
     }
-    TRY(gi::launch_xtr_quant(n, h->T, (int)nb, dR, n, nullptr, 0, qscal, qsum, qimg, partials,
-                             pcap, tickets, h->stream));
+    TRY(gi::launch_xtr_quant(n, h->T, (int)nb, ddesc, qscal, qsum, qimg, partials, pcap, tickets,
+                             h->stream));
     TRY(gi::launch_xtr_mma(d, static_cast<const uint8_t*>(h->gmiss->ptr), miss, (int)nb, qimg,
-                           qscal, qsum, du, dv, static_cast<const int32_t*>(h->s1cnt->ptr),
-                           U ? p : 0, 0, 1.0, h->s_b.as<double>(), p, nullptr, h->sms,
-                           h->stream));
+                           qscal, qsum, ddesc, 1.0, h->sms, h->stream));
     GI_CUDA_TRY(cudaMemcpyAsync(G + b0 * p, h->s_b.mem->ptr, sizeof(double) * nb * p,
                                 cudaMemcpyDeviceToHost, h->stream));
   }

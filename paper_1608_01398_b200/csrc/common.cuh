@@ -196,6 +196,10 @@ int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u,
                      const double* v, const double* d_sum_r, double scale, double* out,
                      cudaStream_t s, double* d_gmax = nullptr, const PubArgs* pub = nullptr,
                      unsigned int* pub_ticket = nullptr, void* pub_out = nullptr);
+// exact gradient on k listed columns, after a fast sweep (aty.cu)
+int launch_support_grad(const MatrixDesc& m, const double* r_pad, const double* u,
+                        const double* v, const double* d_sum_r, double scale, const int64_t* idx,
+                        int64_t k, double* out, double* pub_out, cudaStream_t s);
 int launch_ax(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
               const double* w, int64_t k, double* out, int accumulate, cudaStream_t s);
 // X_S w fused with its image norm (see ax.cu, AxNorm); returns -2 when k is
@@ -215,17 +219,27 @@ int launch_ax_residual(const MatrixDesc& m, const double* u, const double* v,
 int launch_decompress(const MatrixDesc& m, const double* u, const double* v,
                       const int64_t* idx, int64_t k, double* out_t, cudaStream_t s);
 // X^T R on the tensor cores (xtr_mma.cu): the digit image of up to 32
-// residuals (16 with missing genotypes), then one sweep of the 2-bit tiles
+// residuals (16 with missing genotypes), then one sweep of the 2-bit tiles.
+// One descriptor per right-hand side (a device array of them).
+struct XtrRhs {
+  const double* r;          // residual, n entries
+  const uint8_t* keep;      // optional row mask (rows with 0 count as r = 0)
+  const double* u;          // standardisation of this right-hand side (p each)
+  const double* v;
+  const int32_t* s1cnt;     // (sum of doses, observed count) over its rows
+  double* out;              // p outputs: scale_out * v_j (...) as _aty_kernel
+  unsigned long long* gmax; // optional: atomicMax of |out_j / scale_out| (double bits)
+};
+constexpr int kXtrMaxRhs = 32;
 int xtr_mma_cols(int nrhs);
+int xtr_mma_max_rhs(bool any_missing);
 int64_t xtr_mma_qimg_bytes(const MatrixDesc& m, int nrhs);
-int launch_xtr_quant(int64_t n, int64_t T, int nrhs, const double* r, int64_t rstride,
-                     const uint8_t* keep, int64_t kstride, double* qscal, long long* qsum,
-                     int8_t* qimg, double* partials, int64_t partial_cap,
+int launch_xtr_quant(int64_t n, int64_t T, int nrhs, const XtrRhs* d_rhs, double* qscal,
+                     long long* qsum, int8_t* qimg, double* partials, int64_t partial_cap,
                      unsigned int* tickets, cudaStream_t s);
 int launch_xtr_mma(const MatrixDesc& m, const uint8_t* gmiss, bool any_missing, int nrhs,
                    const int8_t* qimg, const double* qscal, const long long* qsum,
-                   const double* u, const double* v, const int32_t* s1cnt, int64_t stat_stride,
-                   int64_t cnt_stride, double scale_out, double* out, int64_t out_stride,
-                   double* gmax, int num_sms, cudaStream_t s, const PubArgs* pub = nullptr,
-                   unsigned int* pub_ticket = nullptr, void* pub_out = nullptr);
+                   const XtrRhs* d_rhs, double scale_out, int num_sms, cudaStream_t s,
+                   const PubArgs* pub = nullptr, unsigned int* pub_ticket = nullptr,
+                   void* pub_out = nullptr);
 }  // namespace gi

@@ -345,7 +345,10 @@ class NativeFit {
     gi::PubArgs pub;
     pub.add(ws_->scal, 8, ws_->oR);
     pub.add(ws_->cvec + ws_->c, ws_->c, ws_->oR + 8);
-    pub.add(ws_->g, ks, ws_->oR + 8 + ws_->c, d_sup);
+    // g on the support: published by the X^T r kernel itself when it is the
+    // exact one; after a fast sweep it is recomputed exactly (and published)
+    // by launch_support_grad below
+    if (exact_) pub.add(ws_->g, ks, ws_->oR + 8 + ws_->c, d_sup);
     if (ws_->p && exact_) {
       // g = -X^T r in the reference's fp64 order (sum r from the residual
       // kernel), then max|g| and the publish
@@ -365,6 +368,11 @@ class NativeFit {
       if (ev1) GI_CUDA_TRY(cudaEventRecord(ev1, s));
       ++aty_launches;
       ++launches;
+      if (ks > 0) {
+        TRY(gi::launch_support_grad(d, ws_->r, ws_->u, ws_->v, ws_->scal + 6, -1.0, d_sup, ks,
+                                    ws_->g, ws_->dmap + ws_->oR + 8 + ws_->c, s));
+        ++launches;
+      }
     }
     if (!ws_->p) {
       if (exact_)  // the centring kernel, skipped here, clears the max|g| slot

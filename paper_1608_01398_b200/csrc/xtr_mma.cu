@@ -201,15 +201,8 @@ struct MmaArgs {
   int nrhs;
   const double* qscal;       // per RHS: scale, mean
   const long long* qsum;     // per RHS: sum of the quantised residual
-  const double* u;
-  const double* v;
-  const int32_t* s1cnt;      // (sum of doses, observed count) per SNP
-  int64_t stat_stride;       // elements between right-hand sides' u / v (0: shared)
-  int64_t cnt_stride;        // int32 pairs between right-hand sides' s1cnt (0: shared)
-  double* out;
-  int64_t out_stride;
+  const XtrRhs* rhs;         // per RHS: stats, output, max|g|
   double scale_out;
-  unsigned long long* gmax;  // optional: atomicMax of |out_j / scale_out| of right-hand side 0
   int64_t n_mtiles;
   long long* prof;           // optional (debug): per-warp phase cycles of CTA 0, 8 per warp
   int dbg;                   // debug (GI_MMA_DBG): bit 0 skip decode, bit 1 skip MMAs,
@@ -360,7 +353,6 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
     uint32_t wph = 0;      // its phase parity
     uint32_t mt_done = 0;  // M-tiles this slot has finished
     int pend = -1;         // A buffer stored but not yet published (afull)
-    double local_max = 0.0;  // max |val| of right-hand side 0 (the IHT loop's max|g|)
     const bool prof = a.prof != nullptr && blockIdx.x == 0 && lane == 0;
     long long pc[4] = {0, 0, 0, 0};  // block wait, done wait, decode + store, epilogue
     long long tp = prof ? clock64() : 0;
@@ -504,25 +496,31 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
           __syncwarp();
           if (lane == 0) bar_arrive(b_dempty + 8 * sl);
         }
-        if (valid && j < m.p) {
 #pragma unroll
-          for (int rb = 0; rb < 2; ++rb) {
-            const int rhs = c0 / 4 + rb;
-            if (rhs < a.nrhs) {
+        for (int rb = 0; rb < 2; ++rb) {
+          const int rhs = c0 / 4 + rb;
+          if (rhs < a.nrhs) {  // warp-uniform
+            const XtrRhs rd = a.rhs[rhs];
+            double val = 0.0;
+            if (valid && j < m.p) {
               const long long Tq = (long long)dd[4 * rb] + 128ll * dd[4 * rb + 1] +
                                    16384ll * dd[4 * rb + 2] + 2097152ll * dd[4 * rb + 3];
               const long long Mq = (long long)mm[4 * rb] + 128ll * mm[4 * rb + 1] +
                                    16384ll * mm[4 * rb + 2] + 2097152ll * mm[4 * rb + 3];
               const double sc = a.qscal[2 * rhs], mean = a.qscal[2 * rhs + 1];
               const double sr = (double)a.qsum[rhs];
-              const double uj = a.u[rhs * a.stat_stride + j];
-              const double vj = a.v[rhs * a.stat_stride + j];
-              const int32_t* cnt = a.s1cnt + 2 * (rhs * a.cnt_stride + j);
-              const double off = (double)cnt[0] - uj * (double)cnt[1];
+              const double uj = rd.u[j], vj = rd.v[j];
+              const double off = (double)rd.s1cnt[2 * j] - uj * (double)rd.s1cnt[2 * j + 1];
               const double inner = (double)Tq + uj * ((double)Mq - sr);
-              const double val = vj * (inner * sc + mean * off);
-              a.out[rhs * a.out_stride + j] = a.scale_out * val;
-              if (rhs == 0) local_max = fmax(local_max, fabs(val));
+              val = vj * (inner * sc + mean * off);
+              rd.out[j] = a.scale_out * val;
+            }
+            if (rd.gmax) {  // max|g| for the IHT step (iht.py:257-261), order-free
+              double mx = fabs(val);
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+              if (lane == 0 && mx > 0.0)
+                atomicMax(rd.gmax, (unsigned long long)__double_as_longlong(mx));
             }
           }
         }
@@ -532,12 +530,6 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
     }
     if (prof)
       for (int q = 0; q < 4; ++q) a.prof[warp * 8 + q] = pc[q];
-    if (a.gmax) {
-      double mx = local_max;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) atomicMax(a.gmax, (unsigned long long)__double_as_longlong(mx));
-    }
   } else {
     // ------------------------------------------------------------ MMA issuers
     const int iw = warp - kDecWarps, sl = iw / ISS, e = iw % ISS;
@@ -633,15 +625,14 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
 // Per right-hand side b (blockIdx.y): over the rows with keep != 0, sum r,
 // count, max r and min r; the last block folds them (block order, fixed tree)
 // into qscal[b] = {s, mean} with s = max|r - mean| / 2^26, and zeroes qsum[b].
-__global__ void xtr_qstats_kernel(int64_t n, const double* __restrict__ r, int64_t rstride,
-                                  const uint8_t* __restrict__ keep, int64_t kstride,
+__global__ void xtr_qstats_kernel(int64_t n, const XtrRhs* __restrict__ rhs,
                                   double* __restrict__ qscal, long long* __restrict__ qsum,
                                   double* __restrict__ partials, unsigned int* __restrict__ ticket) {
   __shared__ double sh[4 * 32];
   __shared__ bool is_last;
   const int b = blockIdx.y;
-  const double* rb = r + b * rstride;
-  const uint8_t* kb = keep ? keep + b * kstride : nullptr;
+  const double* rb = rhs[b].r;
+  const uint8_t* kb = rhs[b].keep;
   double acc[2] = {0.0, 0.0};
   double mx = -INFINITY, mn = INFINITY;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -703,18 +694,19 @@ __global__ void xtr_qstats_kernel(int64_t n, const double* __restrict__ r, int64
 // R_i -> four s8 digits in the chunk image (K order of `selectors`); sum of R_i.
 // Columns of right-hand sides past nrhs are written as zeros.
 template <int N>
-__global__ void xtr_quant_kernel(int64_t n, int64_t n_pad, int nrhs, const double* __restrict__ r,
-                                 int64_t rstride, const uint8_t* __restrict__ keep,
-                                 int64_t kstride, const double* __restrict__ qscal,
+__global__ void xtr_quant_kernel(int64_t n, int64_t n_pad, int nrhs,
+                                 const XtrRhs* __restrict__ rhs, const double* __restrict__ qscal,
                                  long long* __restrict__ qsum, int8_t* __restrict__ qimg) {
   const int b = blockIdx.y;  // right-hand side slot (N / 4 of them)
+  const double* rb = b < nrhs ? rhs[b].r : nullptr;
+  const uint8_t* kb = b < nrhs ? rhs[b].keep : nullptr;
   long long part = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pad;
        i += (int64_t)gridDim.x * blockDim.x) {
     long long R = 0;
-    if (b < nrhs && i < n && (!keep || keep[b * kstride + i])) {
+    if (b < nrhs && i < n && (!kb || kb[i])) {
       const double s = qscal[2 * b], mean = qscal[2 * b + 1];
-      R = __double2ll_rn((r[b * rstride + i] - mean) / s);
+      R = __double2ll_rn((rb[i] - mean) / s);
     }
     part += R;
     const int64_t c = i >> 7;
@@ -764,11 +756,12 @@ int64_t xtr_mma_qimg_bytes(const MatrixDesc& m, int nrhs) {
   return m.T * 4 * 128 * (int64_t)xtr_mma_cols(nrhs);
 }
 
-int launch_xtr_quant(int64_t n, int64_t T, int nrhs, const double* r, int64_t rstride,
-                     const uint8_t* keep, int64_t kstride, double* qscal, long long* qsum,
-                     int8_t* qimg, double* partials, int64_t partial_cap,
+int xtr_mma_max_rhs(bool any_missing) { return any_missing ? 16 : kXtrMaxRhs; }
+
+int launch_xtr_quant(int64_t n, int64_t T, int nrhs, const XtrRhs* d_rhs, double* qscal,
+                     long long* qsum, int8_t* qimg, double* partials, int64_t partial_cap,
                      unsigned int* tickets, cudaStream_t s) {
-  if (nrhs < 1 || nrhs > 32) {
+  if (nrhs < 1 || nrhs > kXtrMaxRhs) {
     gi_set_error("X^T R on the tensor cores takes 1..32 right-hand sides (got %d)", nrhs);
     return -1;
   }
@@ -780,8 +773,7 @@ int launch_xtr_quant(int64_t n, int64_t T, int nrhs, const double* r, int64_t rs
     gi_set_error("internal: quantiser partial buffer too small");
     return -1;
   }
-  xtr_qstats_kernel<<<dim3(blocks, nrhs), 256, 0, s>>>(n, r, rstride, keep, kstride, qscal, qsum,
-                                                      partials, tickets);
+  xtr_qstats_kernel<<<dim3(blocks, nrhs), 256, 0, s>>>(n, d_rhs, qscal, qsum, partials, tickets);
   GI_LAUNCH_CHECK();
   const int N = xtr_mma_cols(nrhs);
   const int64_t n_pad = T * GI_TILE_SAMPLES;
@@ -789,11 +781,11 @@ int launch_xtr_quant(int64_t n, int64_t T, int nrhs, const double* r, int64_t rs
   if (qblocks > 4 * 148) qblocks = 4 * 148;
   const dim3 grid(qblocks, N / 4);
   switch (N) {
-    case 8: xtr_quant_kernel<8><<<grid, 256, 0, s>>>(n, n_pad, nrhs, r, rstride, keep, kstride, qscal, qsum, qimg); break;
-    case 16: xtr_quant_kernel<16><<<grid, 256, 0, s>>>(n, n_pad, nrhs, r, rstride, keep, kstride, qscal, qsum, qimg); break;
-    case 32: xtr_quant_kernel<32><<<grid, 256, 0, s>>>(n, n_pad, nrhs, r, rstride, keep, kstride, qscal, qsum, qimg); break;
-    case 64: xtr_quant_kernel<64><<<grid, 256, 0, s>>>(n, n_pad, nrhs, r, rstride, keep, kstride, qscal, qsum, qimg); break;
-    default: xtr_quant_kernel<128><<<grid, 256, 0, s>>>(n, n_pad, nrhs, r, rstride, keep, kstride, qscal, qsum, qimg); break;
+    case 8: xtr_quant_kernel<8><<<grid, 256, 0, s>>>(n, n_pad, nrhs, d_rhs, qscal, qsum, qimg); break;
+    case 16: xtr_quant_kernel<16><<<grid, 256, 0, s>>>(n, n_pad, nrhs, d_rhs, qscal, qsum, qimg); break;
+    case 32: xtr_quant_kernel<32><<<grid, 256, 0, s>>>(n, n_pad, nrhs, d_rhs, qscal, qsum, qimg); break;
+    case 64: xtr_quant_kernel<64><<<grid, 256, 0, s>>>(n, n_pad, nrhs, d_rhs, qscal, qsum, qimg); break;
+    default: xtr_quant_kernel<128><<<grid, 256, 0, s>>>(n, n_pad, nrhs, d_rhs, qscal, qsum, qimg); break;
   }
   GI_LAUNCH_CHECK();
   return 0;
@@ -801,15 +793,13 @@ int launch_xtr_quant(int64_t n, int64_t T, int nrhs, const double* r, int64_t rs
 
 int launch_xtr_mma(const MatrixDesc& m, const uint8_t* gmiss, bool any_missing, int nrhs,
                    const int8_t* qimg, const double* qscal, const long long* qsum,
-                   const double* u, const double* v, const int32_t* s1cnt, int64_t stat_stride,
-                   int64_t cnt_stride, double scale_out, double* out, int64_t out_stride,
-                   double* gmax, int num_sms, cudaStream_t s, const PubArgs* pub,
-                   unsigned int* pub_ticket, void* pub_out) {
+                   const XtrRhs* d_rhs, double scale_out, int num_sms, cudaStream_t s,
+                   const PubArgs* pub, unsigned int* pub_ticket, void* pub_out) {
   if (m.p == 0) return 0;
   static long long* prof_buf = nullptr;
   const bool prof = getenv("GI_MMA_PROF") != nullptr;
   if (prof && !prof_buf) GI_CUDA_TRY(cudaMallocManaged(&prof_buf, 8 * 32 * sizeof(long long)));
-  if (nrhs < 1 || nrhs > 32 || (any_missing && nrhs > 16)) {
+  if (nrhs < 1 || nrhs > xtr_mma_max_rhs(any_missing)) {
     gi_set_error("X^T R on the tensor cores: %d right-hand sides (1..32, <= 16 with missing "
                  "genotypes)", nrhs);
     return -1;
@@ -821,15 +811,8 @@ int launch_xtr_mma(const MatrixDesc& m, const uint8_t* gmiss, bool any_missing, 
   a.nrhs = nrhs;
   a.qscal = qscal;
   a.qsum = qsum;
-  a.u = u;
-  a.v = v;
-  a.s1cnt = s1cnt;
-  a.stat_stride = stat_stride;
-  a.cnt_stride = cnt_stride;
-  a.out = out;
-  a.out_stride = out_stride;
+  a.rhs = d_rhs;
   a.scale_out = scale_out;
-  a.gmax = reinterpret_cast<unsigned long long*>(gmax);
   a.n_mtiles = (m.G + 3) / 4;
   a.prof = prof ? prof_buf : nullptr;
   a.dbg = getenv("GI_MMA_DBG") ? atoi(getenv("GI_MMA_DBG")) : 0;
@@ -845,8 +828,8 @@ int launch_xtr_mma(const MatrixDesc& m, const uint8_t* gmiss, bool any_missing, 
   int rc;
   if (any_missing) {
     switch (N) {
-      case 8: rc = launch_mma_t<8, 4, true>(a, num_sms, s); break;
-      case 16: rc = launch_mma_t<16, 4, true>(a, num_sms, s); break;
+      case 8: rc = launch_mma_t<8, 2, true>(a, num_sms, s); break;
+      case 16: rc = launch_mma_t<16, 2, true>(a, num_sms, s); break;
       case 32: rc = launch_mma_t<32, 2, true>(a, num_sms, s); break;
       default: rc = launch_mma_t<64, 1, true>(a, num_sms, s); break;
     }
