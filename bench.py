@@ -426,6 +426,7 @@ def secondary(a):
     stream = torch.cuda.current_stream()
 
     def run():
+        ms_mod.LAST_BATCH.clear()
         if a.workload == "c2path":
             res = gi.fit_path(view, y, path)
             return sum(r.iterations for r in res), res
@@ -461,6 +462,8 @@ def secondary(a):
                           "step": "all 41 fits of the path"}
         line["value"] = iters_per_step / (ms / 1e3)
         line["fits_per_s"] = path.size / (ms / 1e3)
+        if ms_mod.LAST_BATCH:
+            line["xtr_batching"] = dict(ms_mod.LAST_BATCH)
         t0 = time.perf_counter()
         want = [oracle.fit(rview, y, int(k)) for k in path]
         t_cpu = time.perf_counter() - t0
@@ -482,9 +485,15 @@ def secondary(a):
         line["config"] = {"workload": f"BASELINE config 4: n={n} x p={p}, 5-fold CV over "
                                       f"k=1..20 + final fit and refit, k_true={k_true}, "
                                       f"fold seed 2016", "step": "one cv_iht call",
-                          "folds": ("compact device copies of the training rows"
+                          "folds": ("row masks over the resident matrix, every (fold, budget) "
+                                    "fit in one lock-step group: their X^T r sweeps batched "
+                                    "as a multi-RHS X^T R on the tensor cores"
+                                    if ms_mod.LAST_BATCH else
+                                    "compact device copies of the training rows"
                                     if ms_mod._compact_folds(m, 5) else
                                     "row masks over the resident matrix")}
+        if ms_mod.LAST_BATCH:
+            line["xtr_batching"] = dict(ms_mod.LAST_BATCH)
         line["value"] = None
         line["cv_seconds"] = ms / 1e3
         line["k_best"] = int(rep.k_best)

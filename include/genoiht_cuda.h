@@ -216,7 +216,8 @@ typedef struct {
   int64_t aty_launches;  /* out: X^T r launches */
   int reason;            /* out: 0 converged, 1 max-iter, 2 step-size collapse */
   int xtr_kernel;        /* out: X^T r kernel the loop ran: 0 exact fp64, 1 fast over the
-                            2-bit tiles, 2 fast over the base-3 copy */
+                            2-bit tiles, 2 fast over the base-3 copy, 3 the lock-step
+                            group's tensor-core sweeps (gi_fit_batched) */
 } gi_fit_result;
 
 /* Replaces genoiht.fit (iht.py:326-354) on one GPU: the complete IHT loop with
@@ -235,6 +236,25 @@ typedef struct {
 int gi_fit(gi_matrix *h, const double *y, const double *C, int64_t c, const uint8_t *keep,
            const double *u, const double *v, const gi_fit_config *cfg, const int64_t *warm_idx,
            const double *warm_w, int64_t warm_k, const double *bcov0, gi_fit_result *res);
+
+/* ------------------------------------------- lock-step groups (multi-RHS) */
+/* Concurrent fits over one matrix (cross-validation folds as row masks, the
+ * budgets of a model-size path) share their X^T r sweeps: gi_fit_batched is
+ * gi_fit whose refresh hands the residual to the group; when every live fit
+ * of the group waits, ONE tensor-core sweep (gi_aty_batched mode 2) serves
+ * all of them (<= 32 residuals, 16 with missing genotypes).  The reference
+ * runs one _aty_kernel sweep per fold fit and iteration (model_select.py:124-139).
+ * A group is tied to the tiles of h (with_stats copies share them).  Fits of a
+ * group must run on separate host threads; results equal each fit's own
+ * tensor-core sweep. */
+typedef struct gi_batch gi_batch;
+int gi_batch_create(gi_matrix *h, int max_rhs, gi_batch **out);
+int gi_batch_stats(const gi_batch *b, int64_t *sweeps, int64_t *rhs);
+int gi_batch_free(gi_batch *b);
+int gi_fit_batched(gi_matrix *h, gi_batch *batch, const double *y, const double *C, int64_t c,
+                   const uint8_t *keep, const double *u, const double *v,
+                   const gi_fit_config *cfg, const int64_t *warm_idx, const double *warm_w,
+                   int64_t warm_k, const double *bcov0, gi_fit_result *res);
 
 /* ------------------------------------------------ SNP-sharded native loop */
 /* One process per GPU, each holding a contiguous SNP block [j_base, j_base +

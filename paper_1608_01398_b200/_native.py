@@ -102,6 +102,11 @@ def _declare(lib):
         "gi_comm_create_nccl": ([P, c_int, c_int, c_int, P], c_int),
         "gi_comm_create_callbacks": ([c_int, c_int, P, P, P, P], c_int),
         "gi_comm_free": ([P], c_int),
+        "gi_batch_create": ([P, c_int, P], c_int),
+        "gi_batch_stats": ([P, P, P], c_int),
+        "gi_batch_free": ([P], c_int),
+        "gi_fit_batched": ([P, P, P, P, c_i64, P, P, P, ctypes.POINTER(FitConfig), P, P, c_i64, P,
+                            ctypes.POINTER(FitOut)], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

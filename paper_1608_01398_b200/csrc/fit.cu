@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/genoiht_cuda.h"
+#include "batch.cuh"
 #include "comm.cuh"
 #include "handle.cuh"
 
@@ -174,9 +175,9 @@ struct Pair {
 class NativeFit {
  public:
   NativeFit(gi_matrix* h, FitWs* ws, const gi_fit_config* cfg, bool masked, double n_eff,
-            gi_comm* comm, int64_t j_base)
+            gi_comm* comm, int64_t j_base, gi_batch* batch = nullptr, cudaEvent_t ready = nullptr)
       : h_(h), ws_(ws), cfg_(*cfg), masked_(masked), n_eff_(n_eff), comm_(comm),
-        j_base_(j_base) {
+        j_base_(j_base), batch_(batch), ready_(ready) {
     // The exact fp64 X^T r kernel -- the reference's own operation order --
     // replaces the fast one where few samples per parameter can amplify the
     // fast kernel's ~6e-7 gradient error past the 1e-6 parity bound (a
@@ -332,6 +333,39 @@ class NativeFit {
       gmax = 0.0;
       gcov.assign(ho + 8, ho + 8 + ws_->c);
       gsup.clear();
+      return 0;
+    }
+    if (batch_ && !exact_ && ws_->p) {
+      // the group's tensor-core sweep computes g (and max|g|) for this fit
+      // together with the other live fits' residuals (batch.cu, xtr_mma.cu)
+      GI_CUDA_TRY(cudaMemsetAsync(ws_->scal + 3, 0, sizeof(double), s));  // max|g| slot
+      gi::XtrRhs rq;
+      rq.r = ws_->r;
+      rq.keep = keep;
+      rq.u = ws_->u;
+      rq.v = ws_->v;
+      rq.s1cnt = ws_->s1cnt;
+      rq.out = ws_->g;
+      rq.gmax = reinterpret_cast<unsigned long long*>(ws_->scal + 3);
+      TRY(gi_batch_submit(batch_, rq, s, ready_));
+      ++aty_launches;
+      gi::PubArgs pub;
+      pub.add(ws_->scal, 8, ws_->oR);
+      pub.add(ws_->cvec + ws_->c, ws_->c, ws_->oR + 8);
+      TRY(gi::launch_publish(pub, ws_->dmap, s));
+      ++launches;
+      const int64_t ks = (int64_t)lsup.size();
+      if (ks > 0) {
+        TRY(gi::launch_support_grad(d, ws_->r, ws_->u, ws_->v, ws_->scal + 6, -1.0, d_sup, ks,
+                                    ws_->g, ws_->dmap + ws_->oR + 8 + ws_->c, s));
+        ++launches;
+      }
+      TRY(sync());
+      const double* ho = ws_->hmap + ws_->oR;
+      loss = ho[0];
+      gmax = ho[3];
+      gcov.assign(ho + 8, ho + 8 + ws_->c);
+      gsup.assign(ho + 8 + ws_->c, ho + 8 + ws_->c + ks);
       return 0;
     }
     if (!exact_) {
@@ -580,6 +614,8 @@ class NativeFit {
   double n_eff_;
   gi_comm* comm_;
   int64_t j_base_;
+  gi_batch* batch_;     // lock-step group of concurrent fits (batch.cu), or NULL
+  cudaEvent_t ready_;   // this fit's residual is ready for the group's sweep
 };
 
 double dot(const std::vector<double>& a) {
@@ -600,7 +636,7 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
                     const double* C, int64_t c, const uint8_t* keep, const double* u,
                     const double* v, const gi_fit_config* cfg, const int64_t* warm_idx,
                     const double* warm_w, int64_t warm_k, const double* bcov0,
-                    gi_fit_result* res) {
+                    gi_fit_result* res, gi_batch* batch = nullptr) {
   const auto t_start = std::chrono::steady_clock::now();
   CHECK_ARG(h && cfg && res, "NULL argument");
   CHECK_ARG(c >= 0 && c <= 64, "the native loop supports at most 64 covariate columns");
@@ -699,7 +735,22 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   ws->n_eff = n_eff;
   }
 
-  NativeFit F(h, ws.get(), cfg, masked, n_eff, comm, j_base);
+  // lock-step group: live from here to the return (every exit path)
+  struct BatchMember {
+    gi_batch* b = nullptr;
+    cudaEvent_t ready = nullptr;
+    ~BatchMember() {
+      if (b) gi_batch_leave(b);
+      if (ready) cudaEventDestroy(ready);
+    }
+  } member;
+  if (batch) {
+    CHECK_ARG(gi_batch_matches(batch, h), "gi_fit_batched: matrix is not the group's");
+    GI_CUDA_TRY(cudaEventCreateWithFlags(&member.ready, cudaEventDisableTiming));
+    TRY(gi_batch_join(batch));
+    member.b = batch;
+  }
+  NativeFit F(h, ws.get(), cfg, masked, n_eff, comm, j_base, batch, member.ready);
   struct EventPair {
     cudaEvent_t a = nullptr, b = nullptr;
     ~EventPair() {
@@ -901,7 +952,7 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
             (long long)iterations, F.syncs, F.sync_us, F.launches,
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start)
                 .count());
-  res->xtr_kernel = F.exact_ ? 0 : (h->desc().x3 != nullptr ? 2 : 1);
+  res->xtr_kernel = F.exact_ ? 0 : (batch ? 3 : (h->desc().x3 != nullptr ? 2 : 1));
   res->kernel_launches = F.launches;
   res->aty_ms_total = F.aty_ms;
   res->aty_launches = F.aty_launches;
@@ -913,6 +964,16 @@ extern "C" int gi_fit(gi_matrix* h, const double* y, const double* C, int64_t c,
                       const gi_fit_config* cfg, const int64_t* warm_idx, const double* warm_w,
                       int64_t warm_k, const double* bcov0, gi_fit_result* res) {
   return fit_impl(h, nullptr, 0, y, C, c, keep, u, v, cfg, warm_idx, warm_w, warm_k, bcov0, res);
+}
+
+extern "C" int gi_fit_batched(gi_matrix* h, gi_batch* batch, const double* y, const double* C,
+                              int64_t c, const uint8_t* keep, const double* u, const double* v,
+                              const gi_fit_config* cfg, const int64_t* warm_idx,
+                              const double* warm_w, int64_t warm_k, const double* bcov0,
+                              gi_fit_result* res) {
+  CHECK_ARG(batch != nullptr, "NULL batch group");
+  return fit_impl(h, nullptr, 0, y, C, c, keep, u, v, cfg, warm_idx, warm_w, warm_k, bcov0, res,
+                  batch);
 }
 
 extern "C" int gi_fit_sharded(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y,

@@ -88,3 +88,52 @@ def test_large_cv_matches_reference(name, compact, monkeypatch):
                                atol=vec_atol(case["final_weights"]))
     np.testing.assert_allclose(rep.final_model.covar, case["final_covar"], rtol=RTOL,
                                atol=1e-12)
+
+
+@pytest.mark.parametrize("name", [k for k in CVS if not LARGE[k]["warm"]])
+def test_large_cv_lockstep_tensor_core_matches_reference(name, monkeypatch):
+    """Cold-start CV with every (fold, budget) fit in one lock-step group: the
+    fits' X^T r sweeps run together on the tensor cores (multi-RHS X^T R,
+    csrc/batch.cu + xtr_mma.cu) -- same golden numbers."""
+    import paper_1608_01398_b200 as gi
+
+    monkeypatch.setenv("GI_BATCH", "1")
+    case = LARGE[name]
+    m = _matrix(case)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=case["n"]))
+    plan = gi.CvPlan.build(case["n"], case["q"], case["path"], seed=case["fold_seed"])
+    from paper_1608_01398_b200.model_select import LAST_BATCH
+
+    LAST_BATCH.clear()
+    rep = gi.cv_iht(view, case["y"], plan, gi.IhtConfig(k=int(case["path"].max())),
+                    std_mode=case["std_mode"], warm_start=False)
+    # the fits' sweeps really were shared: many residuals per sweep
+    assert LAST_BATCH["sweeps"] > 0 and LAST_BATCH["rhs"] >= 4 * LAST_BATCH["sweeps"], LAST_BATCH
+    assert rep.k_best == case["k_best"]
+    np.testing.assert_allclose(rep.mse, case["mse"], rtol=RTOL)
+    np.testing.assert_array_equal(rep.final_model.support, case["final_support"])
+    np.testing.assert_allclose(rep.final_model.weights, case["final_weights"], rtol=RTOL,
+                               atol=vec_atol(case["final_weights"]))
+
+
+@pytest.mark.parametrize("name", [k for k in FITS if LARGE[k]["covar_raw"].size == 0])
+def test_large_path_lockstep_matches_reference(name, monkeypatch):
+    """A model-size path whose budgets run in one lock-step group (one
+    tensor-core sweep per round of refreshes) reproduces the golden fits."""
+    import paper_1608_01398_b200 as gi
+    from paper_1608_01398_b200.iht import BatchGroup
+
+    monkeypatch.setenv("GI_BATCH", "1")
+    case = LARGE[name]
+    m = _matrix(case)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=case["n"]))
+    ks = [int(case["k"]), int(case["k"]) + 3, max(1, int(case["k"]) - 2)]
+    res = gi.fit_path(view, case["y"], sorted(ks))
+    got = res[sorted(ks).index(int(case["k"]))]
+    np.testing.assert_array_equal(got.model.support, case["support"])
+    assert got.iterations == case["iterations"] and got.reason == case["reason"]
+    np.testing.assert_allclose(got.model.weights, case["weights"], rtol=RTOL,
+                               atol=vec_atol(case["weights"]))
+    np.testing.assert_allclose(got.loss_trace, case["loss_trace"], rtol=RTOL, atol=1e-12)
+    with BatchGroup(m) as group:  # stats are reported
+        assert group.stats() == (0, 0)
