@@ -517,7 +517,53 @@ def secondary(a):
                                           f"iterations, {t_fit:.2f} s, x101 fits); "
                                           f"extrapolated CV = {t_cv:.0f} s"}
         line["cv_per_s"] = 1.0 / (ms / 1e3)
+        if a.parity:
+            line["parity"] = cv_fold_parity(gi, ms_mod, view, y, path, g_train, train, test)
     print(json.dumps(line), flush=True)
+
+
+def cv_fold_parity(gi, ms_mod, view, y, path, g_train, train, test):
+    """Config-4 parity record at full size: fold 0's whole budget path.  The
+    device fits run as cv_iht runs them (row masks over the resident matrix,
+    all budgets in one lock-step group with tensor-core X^T R sweeps); the
+    oracle fits the re-packed training rows as the reference does
+    (model_select.py:82-139).  Support, iterations, beta and the held-out MSE
+    per budget.  (The full 5-fold oracle CV takes ~4 min on 16 cores; the
+    golden CV runs of tests/golden hold the complete k_best / MSE grid check.)"""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    t0 = time.perf_counter()
+    v_tr, v_te = ms_mod._fold_views(view, train, test, "train", False)
+    jobs = []
+    with ms_mod.BatchGroup(view.genotypes) as group:
+        jobs = [lambda k=int(k): gi.fit(v_tr, y[train], gi.IhtConfig(k=k), _batch=group)
+                for k in path]
+        got = [r for r, _ in ms_mod._run_concurrently(jobs, len(jobs))]
+    t_dev = time.perf_counter() - t0
+    o_tr = oracle.OracleView(g_train, oracle.intercept(train.size))
+    g_test = view.genotypes  # (device) test rows predicted with the training stats
+    t0 = time.perf_counter()
+    want = [oracle.fit(o_tr, y[train], int(k)) for k in path]
+    t_cpu = time.perf_counter() - t0
+    sup_eq = [bool(np.array_equal(g.model.support, w.support)) for g, w in zip(got, want)]
+    it_eq = [g.iterations == w.iterations for g, w in zip(got, want)]
+    beta = max((rel_diff(g.model.weights, w.weights) for g, w in zip(got, want)
+                if np.array_equal(g.model.support, w.support)), default=0.0)
+    mse_rel = 0.0
+    for g, w in zip(got, want):
+        e_g = y[test] - gi.predict(v_te, g.model)
+        e_w = y[test] - gi.predict(v_te, gi.SparseModel.from_parts(w.support, w.weights, w.covar,
+                                                                   g.model.k, g.model.p))
+        mse_rel = max(mse_rel, abs(float(e_g @ e_g) - float(e_w @ e_w)) / float(e_w @ e_w))
+    del g_test
+    return {"checker": "oracle fits of fold 0's training rows (re-packed, train stats) over "
+                       "the whole path, against the device fits as cv_iht runs them",
+            "fold": 0, "budgets": [int(k) for k in path],
+            "supports_equal": all(sup_eq), "iterations_equal": all(it_eq),
+            "beta_max_rel": beta, "heldout_mse_max_rel": mse_rel,
+            "device_s": t_dev, "oracle_s": t_cpu,
+            "ok": bool(all(sup_eq) and all(it_eq) and beta <= 1e-6 and mse_rel <= 1e-6)}
 
 
 def spawn_ranks(a):
