@@ -149,3 +149,53 @@ def test_reference_cv_dispatches_to_device(dispatched, std_mode):
     atol = RTOL * float(np.max(np.abs(want.final_model.weights)))
     np.testing.assert_allclose(got.final_model.weights, want.final_model.weights, rtol=RTOL,
                                atol=atol)
+
+
+def _report_eq(got, want):
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert (g.k_true, g.snr_divisor, g.replicate) == (w.k_true, w.snr_divisor, w.replicate)
+        assert g.k_selected == w.k_selected
+        assert (g.precision, g.recall) == (w.precision, w.recall)
+        for f in ("mse_test", "h2_true", "h2_est"):
+            np.testing.assert_allclose(getattr(g, f), getattr(w, f), rtol=RTOL)
+
+
+GRID = dict(k_true_grid=[3, 6], snr_divisors=[1.0, 4.0], replicates=2, q=3, path_points=5,
+            seed=11)
+
+
+def test_device_run_experiment_matches_reference(genoiht):
+    """The experiment grid (reference simulate.py:123-186) on the device --
+    paper_1608_01398_b200.run_experiment -- against the reference's own on
+    the host: same selected budgets, precision and recall; MSE and h^2 within
+    1e-6."""
+    import paper_1608_01398_b200 as gi
+
+    n, p = 700, 2400
+    cpu, dev = _pair(genoiht, n, p, 96, 0.01)
+    want = genoiht.run_experiment(genoiht.StandardizedView(cpu, genoiht.CovariateBlock.build(
+        None, n=n)), config=genoiht.IhtConfig(k=12), **GRID)
+    got = gi.run_experiment(gi.StandardizedView(dev, gi.CovariateBlock.build(None, n=n)),
+                            config=gi.IhtConfig(k=12), **GRID)
+    _report_eq(got, want)
+    rows_g, rows_w = gi.aggregate_reports(got), genoiht.aggregate_reports(want)
+    assert [r["k_true"] for r in rows_g] == [r["k_true"] for r in rows_w]
+    for a, b in zip(rows_g, rows_w):
+        np.testing.assert_allclose(a["precision"], b["precision"])
+        np.testing.assert_allclose(a["mse"], b["mse"], rtol=RTOL)
+
+
+def test_reference_run_experiment_on_device_matrix(dispatched):
+    """The reference's OWN run_experiment, unchanged, over a device matrix
+    (its subset_rows / with_stats / cv_iht / predict / heritability reach the
+    B200 through the operator protocol and the installed dispatch)."""
+    genoiht = dispatched
+    n, p = 700, 2400
+    cpu, dev = _pair(genoiht, n, p, 97, 0.0)
+    block = genoiht.CovariateBlock.build(None, n=n)
+    want = genoiht.run_experiment(genoiht.StandardizedView(cpu, block),
+                                  config=genoiht.IhtConfig(k=12), **GRID)
+    got = genoiht.run_experiment(genoiht.StandardizedView(dev, block),
+                                 config=genoiht.IhtConfig(k=12), **GRID)
+    _report_eq(got, want)

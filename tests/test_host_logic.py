@@ -202,3 +202,20 @@ def test_integration_install_dispatches_reference_entry_points(monkeypatch):
         assert genoiht.model_select.fit is ref_fit
     finally:
         sys.path.remove(ref)
+
+
+def test_simulation_helpers_match_reference_definitions():
+    """precision_recall / straddling_path / dense_path (reference
+    simulate.py:95-120) on their edge cases."""
+    import numpy as np
+    import pytest
+
+    import paper_1608_01398_b200 as gi
+
+    assert gi.precision_recall([1, 2, 3], [2, 3, 4]) == (2 / 3, 2 / 3)
+    assert gi.precision_recall([], [5]) == (0.0, 0.0)
+    with pytest.raises(ValueError, match="non-empty"):
+        gi.precision_recall([1], [])
+    np.testing.assert_array_equal(gi.straddling_path(3, 5), [1, 3, 5, 7, 9])
+    np.testing.assert_array_equal(gi.straddling_path(20, 5, 2), [16, 18, 20, 22, 24])
+    np.testing.assert_array_equal(gi.dense_path(2, 3), [1, 2, 3, 4, 5])
