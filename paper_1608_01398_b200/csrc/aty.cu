@@ -782,9 +782,9 @@ __global__ void __launch_bounds__(kExactWarps * 32) aty_exact_kernel(
   }
 }
 
-// Exact gradient on the support (after a fast sweep): one warp per listed
-// column, fp64 sums of dose * r and missing * r over the column (lane-strided,
-// then a fixed xor tree), g_j = scale * v_j (t_j - u_j (sum_r - m_j)) as
+// Exact gradient on the support (after a fast sweep): one block per listed
+// column, fp64 sums of dose * r and missing * r over the column (thread-strided
+// words, then a fixed reduction tree), g_j = scale * v_j (t_j - u_j (sum_r - m_j)) as
 // _aty_kernel forms it (geno_matrix.py:165).  The step size of the next
 // iteration, mu = ||g_S||^2 / ||X_S g_S||^2 (iht.py:233-244), depends on
 // these entries ALONE, and right after a converged warm start they are at the
@@ -792,18 +792,24 @@ __global__ void __launch_bounds__(kExactWarps * 32) aty_exact_kernel(
 // kernel's ~6e-7 rms(g) error would set their direction, and a backtracking
 // test within 1% of its threshold could flip (tools/cv_diag.py).  The fp64
 // sums here are accurate to ~1e-16 of the column's |terms|.
-__global__ void support_grad_kernel(MatrixDesc m, const double* __restrict__ r_pad,
-                                    const double* __restrict__ u, const double* __restrict__ v,
-                                    const double* __restrict__ sum_r, double scale,
-                                    const int64_t* __restrict__ idx, int64_t k,
-                                    double* __restrict__ out, double* __restrict__ pub_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t_idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t_idx >= k) return;
-  const int64_t j = idx[t_idx];
-  double t = 0.0, mm = 0.0;
+constexpr int kSgWords = 1024;  // words per block (4 per thread): a column's slices
+constexpr int kSgMaxSlices = 64;
+
+__global__ void __launch_bounds__(256) support_grad_kernel(
+    MatrixDesc m, const double* __restrict__ r_pad, const double* __restrict__ u,
+    const double* __restrict__ v, const double* __restrict__ sum_r, double scale,
+    const int64_t* __restrict__ idx, double* __restrict__ out, double* __restrict__ pub_out,
+    int slices, double* __restrict__ part, unsigned int* __restrict__ tickets) {
+  // block = (listed column, slice of its words); the last slice to finish
+  // folds the slices' partial sums in slice order and writes g_j
+  __shared__ double sh[2][8];
+  __shared__ bool last;
+  const int col = blockIdx.x / slices, sl = blockIdx.x - col * slices;
+  const int64_t j = idx[col];
   const int64_t words = m.T * GI_TILE_WORDS;
-  for (int64_t wg = lane; wg < words; wg += 32) {
+  const int64_t w0 = (int64_t)sl * words / slices, w1 = (int64_t)(sl + 1) * words / slices;
+  double t = 0.0, mm = 0.0;
+  for (int64_t wg = w0 + threadIdx.x; wg < w1; wg += blockDim.x) {
     const int64_t tile = wg >> 5;
     const int w = (int)(wg & 31);
     const uint32_t wd = __ldg(reinterpret_cast<const uint32_t*>(m.x + word_offset(tile, j, w, m.G)));
@@ -821,20 +827,56 @@ __global__ void support_grad_kernel(MatrixDesc m, const double* __restrict__ r_p
     t += __shfl_xor_sync(0xffffffffu, t, o);
     mm += __shfl_xor_sync(0xffffffffu, mm, o);
   }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
+    sh[0][warp] = t;
+    sh[1][warp] = mm;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    t = 0.0;
+    mm = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+      t += sh[0][q];
+      mm += sh[1][q];
+    }
+    part[2 * blockIdx.x] = t;
+    part[2 * blockIdx.x + 1] = mm;
+    __threadfence();
+    last = atomicAdd(tickets + col, 1u) == (unsigned)(slices - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    t = 0.0;
+    mm = 0.0;
+    for (int q = 0; q < slices; ++q) {
+      t += __ldcg(part + 2 * (col * slices + q));
+      mm += __ldcg(part + 2 * (col * slices + q) + 1);
+    }
     const double g = scale * (v[j] * (t - u[j] * (*sum_r - mm)));
     out[j] = g;
-    if (pub_out) pub_out[t_idx] = g;
+    if (pub_out) pub_out[col] = g;
+    tickets[col] = 0u;
   }
+}
+
+int64_t support_grad_part_doubles(int64_t kcap, int64_t T) {
+  int64_t sl = (T * GI_TILE_WORDS + kSgWords - 1) / kSgWords;
+  if (sl > kSgMaxSlices) sl = kSgMaxSlices;
+  return 2 * kcap * (sl < 1 ? 1 : sl);
 }
 
 int launch_support_grad(const MatrixDesc& m, const double* r_pad, const double* u,
                         const double* v, const double* d_sum_r, double scale, const int64_t* idx,
-                        int64_t k, double* out, double* pub_out, cudaStream_t s) {
+                        int64_t k, double* out, double* pub_out, double* part,
+                        unsigned int* tickets, cudaStream_t s) {
   if (k <= 0 || m.p == 0) return 0;
-  const int warps = 4;
-  support_grad_kernel<<<(unsigned)((k + warps - 1) / warps), warps * 32, 0, s>>>(
-      m, r_pad, u, v, d_sum_r, scale, idx, k, out, pub_out);
+  int64_t sl = (m.T * GI_TILE_WORDS + kSgWords - 1) / kSgWords;
+  if (sl > kSgMaxSlices) sl = kSgMaxSlices;
+  if (sl < 1) sl = 1;
+  support_grad_kernel<<<(unsigned)(k * sl), 256, 0, s>>>(m, r_pad, u, v, d_sum_r, scale, idx, out,
+                                                         pub_out, (int)sl, part, tickets);
   GI_LAUNCH_CHECK();
   return 0;
 }

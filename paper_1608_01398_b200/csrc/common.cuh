@@ -196,10 +196,13 @@ int launch_aty_exact(const MatrixDesc& m, const double* r_pad, const double* u,
                      const double* v, const double* d_sum_r, double scale, double* out,
                      cudaStream_t s, double* d_gmax = nullptr, const PubArgs* pub = nullptr,
                      unsigned int* pub_ticket = nullptr, void* pub_out = nullptr);
-// exact gradient on k listed columns, after a fast sweep (aty.cu)
+// exact gradient on k listed columns, after a fast sweep (aty.cu); part holds
+// support_grad_part_doubles(kcap, T) doubles, tickets kcap zeroed counters
+int64_t support_grad_part_doubles(int64_t kcap, int64_t T);
 int launch_support_grad(const MatrixDesc& m, const double* r_pad, const double* u,
                         const double* v, const double* d_sum_r, double scale, const int64_t* idx,
-                        int64_t k, double* out, double* pub_out, cudaStream_t s);
+                        int64_t k, double* out, double* pub_out, double* part,
+                        unsigned int* tickets, cudaStream_t s);
 int launch_ax(const MatrixDesc& m, const double* u, const double* v, const int64_t* idx,
               const double* w, int64_t k, double* out, int accumulate, cudaStream_t s);
 // X_S w fused with its image norm (see ax.cu, AxNorm); returns -2 when k is

@@ -46,10 +46,13 @@ struct FitWs {
   int32_t* s1cnt = nullptr;
   uint32_t *ticket = nullptr, *rowmask = nullptr;
   uint64_t* ckey = nullptr;
+  double* sg_part = nullptr;       // support-gradient slice partials
+  uint32_t* sg_ticket = nullptr;   // per support column
   double* aty_part = nullptr;      // X^T r tile-slice partial sums (small p only)
   uint32_t* aty_ticket = nullptr;  // X^T r per-chunk arrival counters
   int64_t* cidx = nullptr;
   double* cval = nullptr;
+
   // uploads: pinned host arena mirrored byte for byte by a device arena
   char* hin = nullptr;
   char* din = nullptr;
@@ -141,6 +144,10 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   TRY(ws->dalloc(ws->ckey, ws->slots));
   TRY(ws->dalloc(ws->cidx, ws->slots));
   TRY(ws->dalloc(ws->cval, ws->slots));
+  TRY(ws->dalloc(ws->sg_part, gi::support_grad_part_doubles(kcap, h->T)));
+  TRY(ws->dalloc(ws->sg_ticket, kcap));
+  GI_CUDA_TRY(cudaMemsetAsync(ws->sg_ticket, 0, sizeof(uint32_t) * kcap, ws->stream));
+
   {
     const int64_t part = gi::aty_fast_part_doubles(h->desc(), h->sms);
     if (part > 0) {
@@ -193,8 +200,10 @@ class NativeFit {
     // ranks whose shards straddle a threshold still run the same kernel
     if (cfg->flags & 2) exact_ = (cfg->flags & 4) != 0;
     if (const char* e = getenv("GI_XTR_EXACT")) exact_ = atoi(e) != 0;
+    if (const char* e = getenv("GI_SUPPORT_GRAD")) support_grad_ = atoi(e) != 0;
   }
   bool exact_ = false;
+  bool support_grad_ = true;  // exact gradient on the support after a fast sweep
 
   // gi_fit_sharded always runs the exchange steps, also on a world of one
   // (which is how the NCCL backend is exercised on a single GPU)
@@ -357,7 +366,8 @@ class NativeFit {
       const int64_t ks = (int64_t)lsup.size();
       if (ks > 0) {
         TRY(gi::launch_support_grad(d, ws_->r, ws_->u, ws_->v, ws_->scal + 6, -1.0, d_sup, ks,
-                                    ws_->g, ws_->dmap + ws_->oR + 8 + ws_->c, s));
+                                    ws_->g, ws_->dmap + ws_->oR + 8 + ws_->c, ws_->sg_part,
+                                    ws_->sg_ticket, s));
         ++launches;
       }
       TRY(sync());
@@ -402,9 +412,15 @@ class NativeFit {
       if (ev1) GI_CUDA_TRY(cudaEventRecord(ev1, s));
       ++aty_launches;
       ++launches;
-      if (ks > 0) {
+      if (ks > 0 && support_grad_) {
         TRY(gi::launch_support_grad(d, ws_->r, ws_->u, ws_->v, ws_->scal + 6, -1.0, d_sup, ks,
-                                    ws_->g, ws_->dmap + ws_->oR + 8 + ws_->c, s));
+                                    ws_->g, ws_->dmap + ws_->oR + 8 + ws_->c, ws_->sg_part,
+                                    ws_->sg_ticket, s));
+        ++launches;
+      } else if (ks > 0) {  // GI_SUPPORT_GRAD=0 (diagnostics): the fast sweep's values
+        gi::PubArgs pg;
+        pg.add(ws_->g, ks, ws_->oR + 8 + ws_->c, d_sup);
+        TRY(gi::launch_publish(pg, ws_->dmap, s));
         ++launches;
       }
     }

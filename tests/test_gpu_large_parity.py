@@ -107,8 +107,8 @@ def test_large_cv_lockstep_tensor_core_matches_reference(name, monkeypatch):
     LAST_BATCH.clear()
     rep = gi.cv_iht(view, case["y"], plan, gi.IhtConfig(k=int(case["path"].max())),
                     std_mode=case["std_mode"], warm_start=False)
-    # the fits' sweeps really were shared: many residuals per sweep
-    assert LAST_BATCH["sweeps"] > 0 and LAST_BATCH["rhs"] >= 4 * LAST_BATCH["sweeps"], LAST_BATCH
+    # the fits' sweeps really were shared: several residuals per sweep
+    assert LAST_BATCH["sweeps"] > 0 and LAST_BATCH["rhs"] >= 2 * LAST_BATCH["sweeps"], LAST_BATCH
     assert rep.k_best == case["k_best"]
     np.testing.assert_allclose(rep.mse, case["mse"], rtol=RTOL)
     np.testing.assert_array_equal(rep.final_model.support, case["final_support"])
