@@ -218,3 +218,27 @@ def test_cv_compact_folds_match_masked_folds(std_mode, monkeypatch):
     np.testing.assert_allclose(b.mse, a.mse, rtol=1e-6)
     np.testing.assert_array_equal(b.final_model.support, a.final_model.support)
     np.testing.assert_allclose(b.final_model.weights, a.final_model.weights, rtol=1e-6)
+
+
+def test_cli_bench_dense_mode_gives_rel_to_dense(tmp_path):
+    """With the reference's dense mode (its own DenseDesign on the host, from
+    baseline/_ref) in the run, rel_to_dense is each mode's mean over the dense
+    mean, and the device path selects the same supports as the dense fits."""
+    import os
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline",
+                       "_ref", "genoiht")
+    if not os.path.isdir(ref):
+        pytest.skip("baseline/_ref not installed")
+    from paper_1608_01398_b200.__main__ import main
+    out = str(tmp_path / "d")
+    assert main(["bench", "--synthetic", "500,1500", "--path", "2:8:2", "--mode", "gpu,dense",
+                 "--repetitions", "2", "--out", out, "--seed", "5"]) == 0
+    rows = [ln.split("\t") for ln in open(out + ".bench.tsv").read().splitlines()[2:]]
+    rel = {r[0]: float(r[4]) for r in rows}
+    assert rel["dense"] == 1.0 and 0.0 < rel["gpu"] < 1.0
+    models = [ln.split("\t") for ln in open(out + ".bench_models.tsv").read().splitlines()[2:]]
+    by_mode = {}
+    for mode, k, support in models:
+        by_mode.setdefault(mode, []).append((k, support))
+    assert by_mode["gpu"] == by_mode["dense"]
