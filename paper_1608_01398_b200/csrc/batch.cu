@@ -52,8 +52,9 @@ struct gi_batch {
   int live = 0;
   struct Req {
     gi::XtrRhs rhs;
-    cudaEvent_t ready;
-    int64_t sweep = -1;  // index of the sweep that served it
+    cudaEvent_t ready;   // the fit's residual is ready (recorded on the fit's stream)
+    cudaEvent_t done;    // recorded on the group's stream after the sweep that serves it
+    int64_t sweep = -1;  // index of that sweep (-2: it failed)
   };
   std::deque<Req*> pending;
   // statistics
@@ -99,7 +100,12 @@ struct gi_batch {
     TRY(gi::launch_xtr_mma(desc, static_cast<const uint8_t*>(gmiss_ref->ptr), any_missing, nb,
                            qimg, qscal, qsum, d_desc, -1.0, sms, stream));
     GI_CUDA_TRY(cudaEventRecord(done, stream));
-    for (int b = 0; b < nb; ++b) pending[(size_t)b]->sweep = sweep;
+    for (int b = 0; b < nb; ++b) {
+      // each fit waits on its own event: no aliasing however many sweeps pass
+      // before its thread wakes
+      GI_CUDA_TRY(cudaEventRecord(pending[(size_t)b]->done, stream));
+      pending[(size_t)b]->sweep = sweep;
+    }
     pending.erase(pending.begin(), pending.begin() + nb);
     ++sweeps;
     rhs_total += (uint64_t)nb;
@@ -108,11 +114,13 @@ struct gi_batch {
   }
 };
 
-int gi_batch_submit(gi_batch* b, const gi::XtrRhs& rhs, cudaStream_t s, cudaEvent_t ready) {
+int gi_batch_submit(gi_batch* b, const gi::XtrRhs& rhs, cudaStream_t s, cudaEvent_t ready,
+                    cudaEvent_t done) {
   GI_CUDA_TRY(cudaEventRecord(ready, s));
   gi_batch::Req req;
   req.rhs = rhs;
   req.ready = ready;
+  req.done = done;
   std::unique_lock<std::mutex> lock(b->mu);
   b->pending.push_back(&req);
   if ((int)b->pending.size() >= b->live || (int)b->pending.size() >= b->max_rhs)
@@ -122,7 +130,7 @@ int gi_batch_submit(gi_batch* b, const gi::XtrRhs& rhs, cudaStream_t s, cudaEven
     gi_set_error("batched X^T r sweep failed: %s", gi_last_error());
     return -1;
   }
-  GI_CUDA_TRY(cudaStreamWaitEvent(s, b->events[req.sweep % kEvents], 0));
+  GI_CUDA_TRY(cudaStreamWaitEvent(s, req.done, 0));
   return 0;
 }
 

@@ -182,9 +182,9 @@ struct Pair {
 class NativeFit {
  public:
   NativeFit(gi_matrix* h, FitWs* ws, const gi_fit_config* cfg, bool masked, double n_eff,
-            gi_comm* comm, int64_t j_base, gi_batch* batch = nullptr, cudaEvent_t ready = nullptr)
+            gi_comm* comm, int64_t j_base)
       : h_(h), ws_(ws), cfg_(*cfg), masked_(masked), n_eff_(n_eff), comm_(comm),
-        j_base_(j_base), batch_(batch), ready_(ready) {
+        j_base_(j_base) {
     // The exact fp64 X^T r kernel -- the reference's own operation order --
     // replaces the fast one where few samples per parameter can amplify the
     // fast kernel's ~6e-7 gradient error past the 1e-6 parity bound (a
@@ -356,7 +356,7 @@ class NativeFit {
       rq.s1cnt = ws_->s1cnt;
       rq.out = ws_->g;
       rq.gmax = reinterpret_cast<unsigned long long*>(ws_->scal + 3);
-      TRY(gi_batch_submit(batch_, rq, s, ready_));
+      TRY(gi_batch_submit(batch_, rq, s, ready_, done_));
       ++aty_launches;
       gi::PubArgs pub;
       pub.add(ws_->scal, 8, ws_->oR);
@@ -630,8 +630,13 @@ class NativeFit {
   double n_eff_;
   gi_comm* comm_;
   int64_t j_base_;
-  gi_batch* batch_;     // lock-step group of concurrent fits (batch.cu), or NULL
-  cudaEvent_t ready_;   // this fit's residual is ready for the group's sweep
+
+ public:
+  // lock-step group of concurrent fits (batch.cu), or NULL; only fast-kernel
+  // fits join (an exact-kernel fit never submits a sweep)
+  gi_batch* batch_ = nullptr;
+  cudaEvent_t ready_ = nullptr;  // this fit's residual is ready for the group's sweep
+  cudaEvent_t done_ = nullptr;   // the sweep serving it has completed
 };
 
 double dot(const std::vector<double>& a) {
@@ -751,22 +756,27 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   ws->n_eff = n_eff;
   }
 
+  NativeFit F(h, ws.get(), cfg, masked, n_eff, comm, j_base);
   // lock-step group: live from here to the return (every exit path)
   struct BatchMember {
     gi_batch* b = nullptr;
-    cudaEvent_t ready = nullptr;
+    cudaEvent_t ready = nullptr, done = nullptr;
     ~BatchMember() {
       if (b) gi_batch_leave(b);
       if (ready) cudaEventDestroy(ready);
+      if (done) cudaEventDestroy(done);
     }
   } member;
-  if (batch) {
+  if (batch && !F.exact_ && p > 0) {
     CHECK_ARG(gi_batch_matches(batch, h), "gi_fit_batched: matrix is not the group's");
     GI_CUDA_TRY(cudaEventCreateWithFlags(&member.ready, cudaEventDisableTiming));
+    GI_CUDA_TRY(cudaEventCreateWithFlags(&member.done, cudaEventDisableTiming));
     TRY(gi_batch_join(batch));
     member.b = batch;
+    F.batch_ = batch;
+    F.ready_ = member.ready;
+    F.done_ = member.done;
   }
-  NativeFit F(h, ws.get(), cfg, masked, n_eff, comm, j_base, batch, member.ready);
   struct EventPair {
     cudaEvent_t a = nullptr, b = nullptr;
     ~EventPair() {
@@ -968,7 +978,7 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
             (long long)iterations, F.syncs, F.sync_us, F.launches,
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start)
                 .count());
-  res->xtr_kernel = F.exact_ ? 0 : (batch ? 3 : (h->desc().x3 != nullptr ? 2 : 1));
+  res->xtr_kernel = F.exact_ ? 0 : (F.batch_ ? 3 : (h->desc().x3 != nullptr ? 2 : 1));
   res->kernel_launches = F.launches;
   res->aty_ms_total = F.aty_ms;
   res->aty_launches = F.aty_launches;

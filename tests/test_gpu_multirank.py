@@ -216,7 +216,7 @@ def _path_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_fit_path_on_sharded_view_matches_unsharded_path():
+def test_fit_path_on_sharded_view_matches_unsharded_path(monkeypatch):
     """fit_path over an SNP-sharded view (2 ranks, gloo callbacks, one GPU):
     its fits share the process group's communicator, so they must run
     sequentially; and the X^T r kernel is chosen on the global shape, so the
@@ -237,6 +237,9 @@ def test_fit_path_on_sharded_view_matches_unsharded_path():
 
     y = out[0][1]
     full = gi.PackedGenotypeMatrix.synthetic(1000, 12000, 31)
+    # the unsharded path on the same (lookup-table) kernel -- not in a
+    # tensor-core lock-step group, which sharded fits never use
+    monkeypatch.setenv("GI_BATCH", "0")
     want = gi.fit_path(gi.StandardizedView(full, gi.CovariateBlock.build(None, n=1000)), y,
                        [3, 8, 12])
     for _, _, fits in out:
