@@ -14,7 +14,9 @@
 // in a backtracking phase, which needs no sweep) never holds the others for
 // longer than its own phase.  Results equal the single-RHS tensor-core sweep
 // of each fit: per-RHS integer sums do not interact.
+#include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <deque>
 #include <mutex>
 #include <vector>
@@ -34,6 +36,7 @@ struct gi_batch {
   std::shared_ptr<DevMem> gmiss_ref;
   bool any_missing = false;
   int max_rhs = 32;
+  int wait_us = 0;  // optional straggler bound (GI_BATCH_WAIT_US), 0 = none
   cudaStream_t stream = nullptr;
   // device scratch, reused by consecutive sweeps in stream order
   gi::XtrRhs* d_desc = nullptr;
@@ -125,7 +128,20 @@ int gi_batch_submit(gi_batch* b, const gi::XtrRhs& rhs, cudaStream_t s, cudaEven
   b->pending.push_back(&req);
   if ((int)b->pending.size() >= b->live || (int)b->pending.size() >= b->max_rhs)
     b->launch_locked();  // failure is reported through req.sweep
-  b->cv.wait(lock, [&] { return req.sweep != -1; });
+  // Optional straggler bound (GI_BATCH_WAIT_US): a waiter that has waited
+  // that long without a sweep launches what has gathered.  Off by default:
+  // at config 4, 100 / 300 / 1000 us gave 0.60-0.65 / 0.42-0.47 / 0.39-0.54 s
+  // (240 / 180 / 140 sweeps for 713 residuals) against ~0.27-0.48 s with ~40
+  // sweeps when every live fit is waited for.
+  while (req.sweep == -1) {
+    if (b->wait_us <= 0) {
+      b->cv.wait(lock);
+    } else if (b->cv.wait_for(lock, std::chrono::microseconds(b->wait_us)) ==
+                   std::cv_status::timeout &&
+               req.sweep == -1 && !b->pending.empty()) {
+      b->launch_locked();
+    }
+  }
   if (req.sweep < 0) {
     gi_set_error("batched X^T r sweep failed: %s", gi_last_error());
     return -1;
@@ -175,6 +191,7 @@ int gi_batch_create(gi_matrix* h, int max_rhs, gi_batch** out) {
     }
     for (uint8_t f : flags) b->any_missing |= f != 0;
   }
+  if (const char* w = getenv("GI_BATCH_WAIT_US")) b->wait_us = atoi(w);
   const int cap = gi::xtr_mma_max_rhs(b->any_missing);
   b->max_rhs = max_rhs > 0 && max_rhs < cap ? max_rhs : cap;
   auto fail = [&](cudaError_t e) {

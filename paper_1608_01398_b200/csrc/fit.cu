@@ -254,9 +254,20 @@ class NativeFit {
   }
   double sync_us = 0.0;
   int syncs = 0;
-  int sync() {
+  // Lock-step groups run up to 32 fits on as many host threads; a fit waiting
+  // on the group's sweep (the refresh, ~1 ms) sleeps on a blocking-sync event
+  // so the waiting threads do not oversubscribe the host cores.  Every other
+  // phase spins, as a single fit does: blocking on all of them cost 2-5x at
+  // config 2 (wake-up latency per short phase).
+  cudaEvent_t block_ev_ = nullptr;
+  int sync(bool blocking = false) {
     const auto t0 = std::chrono::steady_clock::now();
-    GI_CUDA_TRY(cudaStreamSynchronize(ws_->stream));
+    if (block_ev_ && blocking) {
+      GI_CUDA_TRY(cudaEventRecord(block_ev_, ws_->stream));
+      GI_CUDA_TRY(cudaEventSynchronize(block_ev_));
+    } else {
+      GI_CUDA_TRY(cudaStreamSynchronize(ws_->stream));
+    }
     sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
                    .count();
     ++syncs;
@@ -370,7 +381,7 @@ class NativeFit {
                                     ws_->sg_ticket, s));
         ++launches;
       }
-      TRY(sync());
+      TRY(sync(true));  // waits on the group's sweep (~1 ms): sleep, don't spin
       const double* ho = ws_->hmap + ws_->oR;
       loss = ho[0];
       gmax = ho[3];
@@ -760,11 +771,12 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   // lock-step group: live from here to the return (every exit path)
   struct BatchMember {
     gi_batch* b = nullptr;
-    cudaEvent_t ready = nullptr, done = nullptr;
+    cudaEvent_t ready = nullptr, done = nullptr, block = nullptr;
     ~BatchMember() {
       if (b) gi_batch_leave(b);
       if (ready) cudaEventDestroy(ready);
       if (done) cudaEventDestroy(done);
+      if (block) cudaEventDestroy(block);
     }
   } member;
   if (batch && !F.exact_ && p > 0) {
@@ -776,6 +788,9 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
     F.batch_ = batch;
     F.ready_ = member.ready;
     F.done_ = member.done;
+    GI_CUDA_TRY(cudaEventCreateWithFlags(&member.block,
+                                         cudaEventBlockingSync | cudaEventDisableTiming));
+    F.block_ev_ = member.block;
   }
   struct EventPair {
     cudaEvent_t a = nullptr, b = nullptr;

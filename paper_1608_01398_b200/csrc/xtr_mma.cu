@@ -61,6 +61,13 @@ constexpr int kChunkSamples = 128;  // one MMA chunk: 8 words, 32 TMEM columns, 
 // > half the SM, so one CTA per SM owns all of TMEM
 constexpr int kSmemMma = 200 * 1024;
 constexpr uint32_t kDoseLut = 0x02010000u;  // code 0, 1, 2, 3 -> dose 0, 0, 1, 2
+// per-warp phase timers of CTA 0 (GI_MMA_PROF=1 at run time), compiled in
+// only with -DGI_MMA_PROFILE: they cost issue slots in the decode loop
+#ifdef GI_MMA_PROFILE
+constexpr bool kMmaProfile = true;
+#else
+constexpr bool kMmaProfile = false;
+#endif
 constexpr uint32_t kMissLut = 0x00000100u;  // code 1 (missing) -> 1
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -205,8 +212,6 @@ struct MmaArgs {
   double scale_out;
   int64_t n_mtiles;
   long long* prof;           // optional (debug): per-warp phase cycles of CTA 0, 8 per warp
-  int dbg;                   // debug (GI_MMA_DBG): bit 0 skip decode, bit 1 skip MMAs,
-                             // bit 2 skip the chunk handshakes (wrong results)
   PubArgs pub;               // optional publish by the last CTA (native IHT loop)
   unsigned int* pub_ticket;
   unsigned long long* pub_out;
@@ -353,8 +358,9 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
     uint32_t wph = 0;      // its phase parity
     uint32_t mt_done = 0;  // M-tiles this slot has finished
     int pend = -1;         // A buffer stored but not yet published (afull)
-    const bool prof = a.prof != nullptr && blockIdx.x == 0 && lane == 0;
-    long long pc[4] = {0, 0, 0, 0};  // block wait, done wait, decode + store, epilogue
+    const bool prof = kMmaProfile && a.prof != nullptr && blockIdx.x == 0 && lane == 0;
+    // block wait, done wait, block loads + refill, decode, stores + publish, other, epilogue
+    long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tp = prof ? clock64() : 0;
     auto tick = [&](int q) {
       if (prof) {
@@ -379,7 +385,7 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
         const uint32_t s = bt % kBlkSlots;
         uint32_t wd[32];
         if (valid) {
-          tick(2);
+          tick(5);
           bar_wait(myb + 8 * s, (bt / kBlkSlots) & 1u);
           tick(0);
           ++bt;
@@ -392,21 +398,14 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
                          : "r"(base + (uint32_t)((lane ^ w) << 7)));
             wd[w] = x;
           }
-          // the generic reads above precede the async-proxy refill of the slot
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0 && t + kBlkSlots < T) {
-            bar_arrive_tx(myb + 8 * s, GI_BLOCK_BYTES);
-            bulk_g2s(slot0 + s * GI_BLOCK_BYTES, src + (t + kBlkSlots) * tile_stride,
-                     GI_BLOCK_BYTES, myb + 8 * s);
-          }
+          tick(2);
         }
 #pragma unroll
         for (int hq = 0; hq < 4; ++hq) {
-          if (ci >= (uint32_t)NB && (ci % C::kCB) == 0 && !(a.dbg & 4)) {
+          if (ci >= (uint32_t)NB && (ci % C::kCB) == 0) {
             // chunks ci - NB .. ci - NB + kCB - 1 consumed (one commit group):
             // their A buffers and digit slots are free
-            tick(2);
+            tick(5);
             bar_wait(b_done + 8 * (sl * R + wr + C::kCB - 1), wph);
             tick(1);
             wr += C::kCB;
@@ -417,7 +416,8 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
           }
           tc_fence_after();
           if (digit_lane) issue_digits();
-          if (valid && !(a.dbg & 1)) {
+          tick(5);
+          if (valid) {
             // decode the chunk into registers, then publish the PREVIOUS chunk
             // (its stores have had this decode to land: the ~130-cycle
             // store -> wait::st latency stays off the critical path), then
@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
             for (int q = 0; q < 4; ++q) selectors(wd[8 * hq + 4 + q], sel[q]);
             lut16(sel, dose_lut, zero, o2);
             if (MISS && miss) lut16(sel, miss_lut, zero, m2);
+            tick(3);
             if (C::kDefer && pend >= 0) {
               asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
               tc_fence_before();
@@ -456,8 +457,22 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
             __syncwarp();
             if (lane == 0) bar_arrive(b_afull + 8 * (sl * NB + wb));
           }
+          tick(4);
           ++ci;
           wb = wb + 1 == (uint32_t)NB ? 0u : wb + 1;
+        }
+        // refill the tile's slot only now: every loaded word has been consumed
+        // by the decode (a register dependency), so the generic reads are
+        // complete before the async-proxy write -- no proxy fence needed, and
+        // kBlkSlots - 1 tiles stay in flight
+        if (valid) {
+          __syncwarp();
+          if (lane == 0 && t + kBlkSlots < T) {
+            const uint32_t s2 = (bt - 1) % kBlkSlots;
+            bar_arrive_tx(myb + 8 * s2, GI_BLOCK_BYTES);
+            bulk_g2s(slot0 + s2 * GI_BLOCK_BYTES, src + (t + kBlkSlots) * tile_stride,
+                     GI_BLOCK_BYTES, myb + 8 * s2);
+          }
         }
       }
       if (pend >= 0) {  // publish the M-tile's last chunk
@@ -468,7 +483,7 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
         pend = -1;
       }
       // ---------------------------------------------------------- epilogue
-      tick(2);
+      tick(5);
       bar_wait(b_dfull + 8 * sl, mt_done & 1u);
       tc_fence_after();
       const int64_t j = g * 32 + lane;
@@ -526,15 +541,15 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
         }
       }
       ++mt_done;
-      tick(3);
+      tick(6);
     }
     if (prof)
-      for (int q = 0; q < 4; ++q) a.prof[warp * 8 + q] = pc[q];
+      for (int q = 0; q < 8; ++q) a.prof[warp * 8 + q] = pc[q];
   } else {
     // ------------------------------------------------------------ MMA issuers
     const int iw = warp - kDecWarps, sl = iw / ISS, e = iw % ISS;
     if (lane == 0) {
-      const bool prof = a.prof != nullptr && blockIdx.x == 0;
+      const bool prof = kMmaProfile && a.prof != nullptr && blockIdx.x == 0;
       long long pc[4] = {0, 0, 0, 0};  // afull wait, bfull wait, MMA + commit, dempty wait
       long long tp = prof ? clock64() : 0;
       auto tick = [&](int q) {
@@ -559,7 +574,7 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
         const uint32_t dcol = tmem + (uint32_t)(C::kAtot + (sl * ISS + e) * C::kDcols);
         for (uint32_t c = 0; c < nchunks; ++c) {
           tick(2);
-          if (!(a.dbg & 4)) bar_wait(b_afull + 8 * (sl * NB + b), bph);
+          bar_wait(b_afull + 8 * (sl * NB + b), bph);
           tick(0);
           bar_wait(b_bfull + 8 * (sl * R + r), rph);
           tick(1);
@@ -573,10 +588,8 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
                                    ((uint64_t)((C::kLBO >> 4) & 0x3FFF) << 16) |
                                    ((uint64_t)((C::kSBO >> 4) & 0x3FFF) << 32) | (1ull << 46);
             const uint32_t acc = (c > 0 || ks != e) ? 1u : 0u;
-            if (!(a.dbg & 2)) {
-              mma_i8(dcol, acol + 8u * ks, bdesc, C::kIdesc, acc);
-              if (MISS && miss) mma_i8(dcol + N, acol + 32u + 8u * ks, bdesc, C::kIdesc, acc);
-            }
+            mma_i8(dcol, acol + 8u * ks, bdesc, C::kIdesc, acc);
+            if (MISS && miss) mma_i8(dcol + N, acol + 32u + 8u * ks, bdesc, C::kIdesc, acc);
           }
           if ((c % C::kCB) == C::kCB - 1) mma_commit(b_done + 8 * (sl * R + r));
           if (++b == (uint32_t)NB) {
@@ -815,7 +828,6 @@ int launch_xtr_mma(const MatrixDesc& m, const uint8_t* gmiss, bool any_missing, 
   a.scale_out = scale_out;
   a.n_mtiles = (m.G + 3) / 4;
   a.prof = prof ? prof_buf : nullptr;
-  a.dbg = getenv("GI_MMA_DBG") ? atoi(getenv("GI_MMA_DBG")) : 0;
   if (pub && pub_ticket && pub_out) {
     a.pub = *pub;
     a.pub_ticket = pub_ticket;
@@ -845,8 +857,9 @@ int launch_xtr_mma(const MatrixDesc& m, const uint8_t* gmiss, bool any_missing, 
   if (prof && rc == 0) {
     GI_CUDA_TRY(cudaStreamSynchronize(s));
     for (int w = 0; w < 16; ++w)
-      fprintf(stderr, "mma prof warp %2d: %12lld %12lld %12lld %12lld\n", w, prof_buf[w * 8],
-              prof_buf[w * 8 + 1], prof_buf[w * 8 + 2], prof_buf[w * 8 + 3]);
+      fprintf(stderr, "mma prof warp %2d: %11lld %11lld %11lld %11lld %11lld %11lld %11lld\n", w,
+              prof_buf[w * 8], prof_buf[w * 8 + 1], prof_buf[w * 8 + 2], prof_buf[w * 8 + 3],
+              prof_buf[w * 8 + 4], prof_buf[w * 8 + 5], prof_buf[w * 8 + 6]);
   }
   return rc;
 }
