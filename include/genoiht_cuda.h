@@ -92,6 +92,10 @@ int gi_matrix_device_stats(const gi_matrix *h, const double **d_u, const double 
 /* column statistics over the rows with keep[i] != 0 (host in, length n):
  * the u, v that subset_rows(rows) would compute, without re-packing */
 int gi_matrix_masked_stats(const gi_matrix *h, const uint8_t *keep, double *u, double *v);
+/* a copy of h (same tiles) standardised with those statistics, computed on the
+ * device (no host round trip): a CV fold's matrix in train mode
+ * (model_select.py:87-93) */
+int gi_matrix_with_masked_stats(const gi_matrix *h, const uint8_t *keep, gi_matrix **out);
 
 /* ------------------------------------------------ operator protocol (host) */
 /* aty_genetic (geno_matrix.py:351-364).  mode 0: exact -- bit-identical to
@@ -215,6 +219,8 @@ typedef struct {
   double aty_ms_total;   /* out: summed X^T r kernel time (flags bit 0) */
   int64_t aty_launches;  /* out: X^T r launches */
   int reason;            /* out: 0 converged, 1 max-iter, 2 step-size collapse */
+  double heldout_sse;    /* out: sum over the rows with keep == 2 of (y - X_S b - C b_cov)^2 */
+  int64_t heldout_n;     /* out: their count */
   int xtr_kernel;        /* out: X^T r kernel the loop ran: 0 exact fp64, 1 fast over the
                             2-bit tiles, 2 fast over the base-3 copy, 3 the lock-step
                             group's tensor-core sweeps (gi_fit_batched) */
@@ -223,8 +229,10 @@ typedef struct {
 /* Replaces genoiht.fit (iht.py:326-354) on one GPU: the complete IHT loop with
  * device kernels, one host sync per phase.  y (n) and C (row-major n x c,
  * c <= 64) are host arrays over the handle's n samples; keep (n, optional)
- * restricts the fit to rows with keep != 0 (cross-validation training rows:
- * other rows' residuals are pinned to 0); u, v (p, optional) override the
+ * restricts the fit to rows with keep == 1 (cross-validation training rows:
+ * other rows' residuals are pinned to 0); rows with keep == 2 are held out and
+ * scored after the fit (heldout_sse / heldout_n: the fold's test rows,
+ * model_select.py:138-139); u, v (p, optional) override the
  * handle's stats; warm_idx/warm_w (warm_k, sorted, may be NULL) seed the
  * support; bcov0 (c) is the initial covariate block (least squares on the
  * caller side, as in initial_state iht.py:207-208).  y == NULL reuses the y, C,

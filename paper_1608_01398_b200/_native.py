@@ -47,7 +47,8 @@ class FitOut(ctypes.Structure):
                 ("covar", c_vp), ("loss_trace", c_vp), ("trace_cap", c_i64),
                 ("trace_len", c_i64), ("iterations", c_i64), ("backtracks", c_i64),
                 ("kernel_launches", c_i64), ("aty_ms_total", c_dbl), ("aty_launches", c_i64),
-                ("reason", c_int), ("xtr_kernel", c_int)]
+                ("reason", c_int), ("heldout_sse", c_dbl), ("heldout_n", c_i64),
+                ("xtr_kernel", c_int)]
 
 
 def _declare(lib):
@@ -102,6 +103,7 @@ def _declare(lib):
         "gi_comm_create_nccl": ([P, c_int, c_int, c_int, P], c_int),
         "gi_comm_create_callbacks": ([c_int, c_int, P, P, P, P], c_int),
         "gi_comm_free": ([P], c_int),
+        "gi_matrix_with_masked_stats": ([P, P, P], c_int),
         "gi_batch_create": ([P, c_int, P], c_int),
         "gi_batch_stats": ([P, P, P], c_int),
         "gi_batch_free": ([P], c_int),

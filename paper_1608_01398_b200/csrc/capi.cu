@@ -345,6 +345,46 @@ int gi_matrix_masked_stats(const gi_matrix* hc, const uint8_t* keep, double* u, 
   return 0;
 }
 
+// A copy of src (same tiles) standardised with the statistics of the rows
+// with keep != 0, computed on the device -- subset_rows(rows).u / .v without
+// the host round trip of gi_matrix_masked_stats + gi_matrix_with_stats (CV
+// folds in train mode, model_select.py:87-93).
+int gi_matrix_with_masked_stats(const gi_matrix* srcc, const uint8_t* keep, gi_matrix** out) {
+  gi_matrix* src = const_cast<gi_matrix*>(srcc);
+  CHECK_ARG(src && keep && out, "NULL argument");
+  std::vector<uint32_t> mask;
+  build_rowmask(src, keep, mask);
+  std::unique_ptr<gi_matrix> h(new gi_matrix());
+  h->device = src->device;
+  h->sms = src->sms;
+  h->n = src->n;
+  h->p = src->p;
+  h->nb = src->nb;
+  h->T = src->T;
+  h->G = src->G;
+  h->x = src->x;
+  h->x3 = src->x3;
+  h->T3 = src->T3;
+  h->miss_cnt = src->miss_cnt;
+  h->gmiss = src->gmiss;
+  h->s1cnt = src->s1cnt;
+  h->any_missing = src->any_missing;
+  DeviceGuard g(h->device);
+  GI_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  TRY(alloc(h->u, sizeof(double) * std::max<int64_t>(h->p, 1), h->device, true));
+  TRY(alloc(h->v, sizeof(double) * std::max<int64_t>(h->p, 1), h->device, true));
+  if (h->p > 0) {
+    TRY(h->s_a.ensure(mask.size() * 4, h->device));
+    GI_CUDA_TRY(cudaMemcpyAsync(h->s_a.mem->ptr, mask.data(), mask.size() * 4,
+                                cudaMemcpyHostToDevice, h->stream));
+    TRY(gi::launch_stats(h->desc(), h->s_a.as<uint32_t>(), h->du(), h->dv(), nullptr, nullptr,
+                         h->stream));
+    GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  *out = h.release();
+  return 0;
+}
+
 // ------------------------------------------------------- host-buffer operators
 // One aty_genetic sweep on h's stream (caller holds h->mu and the device):
 // r, out on the host; u, v device pointers (the handle's or caller stats).

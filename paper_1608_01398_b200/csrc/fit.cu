@@ -43,6 +43,7 @@ struct FitWs {
   double *u = nullptr, *v = nullptr;
   float* rt = nullptr;
   uint8_t* keep = nullptr;
+  uint8_t* keep_test = nullptr;  // held-out rows scored at the end (keep == 2 on input)
   int32_t* s1cnt = nullptr;
   uint32_t *ticket = nullptr, *rowmask = nullptr;
   uint64_t* ckey = nullptr;
@@ -100,7 +101,13 @@ struct FitPool {
   std::mutex mu;
   std::vector<std::shared_ptr<FitWs>> items;
 };
-constexpr size_t kPoolCap = 32;
+// Enough for a lock-step group of concurrent fits (model_select._group_workers)
+// plus the final fit: an eviction frees device memory, which synchronises the
+// device under every other fit in flight.
+constexpr size_t kPoolCap = 64;
+// Workspace shapes are rounded up to whole multiples of this many support
+// slots, so the fits of one path / CV (k = 1..20, say) share one shape.
+constexpr int64_t kKcapQuantum = 32;
 
 FitPool& fit_pool_for(int device) {
   static std::mutex mu;
@@ -138,6 +145,7 @@ int make_ws(gi_matrix* h, int64_t c, int64_t kcap, std::shared_ptr<FitWs>& out) 
   TRY(ws->dalloc(ws->v, p));
   TRY(ws->dalloc(ws->rt, ws->npad));
   TRY(ws->dalloc(ws->keep, n));
+  TRY(ws->dalloc(ws->keep_test, n));
   TRY(ws->dalloc(ws->s1cnt, 2 * p));
   TRY(ws->dalloc(ws->ticket, 1));
   TRY(ws->dalloc(ws->rowmask, ws->npad / 16));
@@ -621,6 +629,39 @@ class NativeFit {
     return 0;
   }
 
+  // sum over the held-out rows of (y - X_S w - C bcov)^2 (ws keep_test)
+  int score(const std::vector<int64_t>& sup, const std::vector<double>& w,
+            const std::vector<double>& bcov, double& sse) {
+    const gi::MatrixDesc d = h_->desc();
+    cudaStream_t s = ws_->stream;
+    const int64_t* d_sup = nullptr;
+    const double *d_w = nullptr, *d_cov = nullptr;
+    TRY(stage(sup.data(), (int64_t)sup.size(), d_sup));
+    TRY(stage(w.data(), (int64_t)w.size(), d_w));
+    TRY(stage(bcov.data(), ws_->c, d_cov));
+    TRY(flush());
+    int rc = gi::launch_ax_residual(d, ws_->u, ws_->v, d_sup, d_w, (int64_t)sup.size(), ws_->y,
+                                    ws_->c ? ws_->C : nullptr, (int)ws_->c, d_cov, ws_->keep_test,
+                                    1.0, ws_->r, ws_->scal, nullptr, 0, nullptr, nullptr,
+                                    ws_->beta, ws_->partials, ws_->ticket, s);
+    if (rc != 0 && rc != -2) return -1;
+    if (rc == -2) {
+      if (!sup.empty())
+        TRY(gi::launch_ax(d, ws_->u, ws_->v, d_sup, d_w, (int64_t)sup.size(), ws_->fitb, 0, s));
+      TRY(gi::launch_refresh_residual(ws_->n, ws_->y, sup.empty() ? nullptr : ws_->fitb,
+                                      ws_->c ? ws_->C : nullptr, (int)ws_->c, d_cov,
+                                      ws_->keep_test, 1.0, ws_->r, ws_->scal, nullptr, 0, nullptr,
+                                      nullptr, ws_->beta, ws_->partials, ws_->ticket, s));
+    }
+    gi::PubArgs pub;
+    pub.add(ws_->scal, 1, ws_->oR);
+    TRY(gi::launch_publish(pub, ws_->dmap, s));
+    TRY(sync());
+    sse = 2.0 * ws_->hmap[ws_->oR];  // scal[0] = 0.5 sum r^2 over the scored rows
+    launches += 3;
+    return 0;
+  }
+
   int scatter_beta(const std::vector<int64_t>& idx_g, const std::vector<double>& w_g) {
     std::vector<int64_t> idx;
     std::vector<double> w;
@@ -677,7 +718,8 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   CHECK_ARG(res->trace_cap >= cfg->max_iter + 1, "loss trace buffer is too small");
   CHECK_ARG(res->support_cap >= std::max<int64_t>(cfg->k, warm_k), "support buffer too small");
   DeviceGuard guard(h->device);
-  const int64_t kcap = std::max<int64_t>(std::max<int64_t>(cfg->k, warm_k), 1);
+  const int64_t kneed = std::max<int64_t>(std::max<int64_t>(cfg->k, warm_k), 1);
+  const int64_t kcap = (kneed + kKcapQuantum - 1) / kKcapQuantum * kKcapQuantum;
 
   // take a workspace of the right shape from the device's pool (or make one);
   // y == NULL (resident inputs) needs one primed by an earlier call on h
@@ -685,15 +727,19 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   std::shared_ptr<FitWs> ws;
   {
     std::lock_guard<std::mutex> lock(pool.mu);
+    // the tightest fit, most recently returned first among equals
     auto& items = pool.items;
-    for (size_t i = items.size(); i-- > 0;) {  // most recently returned first
+    size_t best = items.size();
+    for (size_t i = items.size(); i-- > 0;) {
       const auto& cand = items[i];
-      if (cand->c == c && cand->kcap >= kcap && cand->n == h->n && cand->p == h->p &&
-          (y != nullptr || (cand->primed && cand->primed_uid == h->uid))) {
-        ws = cand;
-        items.erase(items.begin() + (long)i);
-        break;
-      }
+      if (cand->c == c && cand->kcap >= kneed && cand->n == h->n && cand->p == h->p &&
+          (y != nullptr || (cand->primed && cand->primed_uid == h->uid)) &&
+          (best == items.size() || cand->kcap < items[best]->kcap))
+        best = i;
+    }
+    if (best != items.size()) {
+      ws = items[best];
+      items.erase(items.begin() + (long)best);
     }
   }
   if (!ws) {
@@ -722,6 +768,7 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   }
   const int64_t n = h->n, p = h->p;
   double n_eff = (double)n;
+  int64_t n_test = 0;  // held-out rows (keep == 2) of this call
   const bool masked = keep != nullptr || (y == nullptr && ws->masked);
   const gi::MatrixDesc d = h->desc();
   if (y == nullptr) {
@@ -735,14 +782,24 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   GI_CUDA_TRY(cudaMemcpyAsync(ws->y, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
   if (c) GI_CUDA_TRY(cudaMemcpyAsync(ws->C, C, sizeof(double) * n * c, cudaMemcpyHostToDevice, s));
   if (masked) {
-    GI_CUDA_TRY(cudaMemcpyAsync(ws->keep, keep, (size_t)n, cudaMemcpyHostToDevice, s));
+    // keep: 1 = a fit row, 2 = a held-out row scored after the fit, 0 = neither
+    std::vector<uint8_t> fit_rows((size_t)n), test_rows((size_t)n);
     std::vector<uint32_t> mask((size_t)(ws->npad / 16), 0u);
     int64_t cnt = 0;
-    for (int64_t i = 0; i < n; ++i)
-      if (keep[i]) {
+    n_test = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      fit_rows[(size_t)i] = keep[i] == 1;
+      test_rows[(size_t)i] = keep[i] == 2;
+      n_test += keep[i] == 2;
+      if (keep[i] == 1) {
         mask[(size_t)(i >> 4)] |= 1u << (2 * (i & 15));
         ++cnt;
       }
+    }
+    GI_CUDA_TRY(cudaMemcpyAsync(ws->keep, fit_rows.data(), (size_t)n, cudaMemcpyHostToDevice, s));
+    if (n_test)
+      GI_CUDA_TRY(cudaMemcpyAsync(ws->keep_test, test_rows.data(), (size_t)n,
+                                  cudaMemcpyHostToDevice, s));
     n_eff = (double)cnt;
     GI_CUDA_TRY(cudaMemcpyAsync(ws->rowmask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice,
                                 s));
@@ -972,6 +1029,12 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
       break;
     }
   }
+  // ---- held-out score (cross-validation: the fold's test rows, standardised
+  // with the fit's own statistics, model_select.py:138-139): sum over the
+  // test rows of (y - X_S b - C b_cov)^2, in the fused residual kernel
+  res->heldout_n = n_test;
+  res->heldout_sse = 0.0;
+  if (n_test > 0 && comm == nullptr) TRY(F.score(sup, w, bcov, res->heldout_sse));
   // ---- model (SparseModel.from_parts: nonzero weights, sorted)
   int64_t nnz = 0;
   for (size_t t = 0; t < sup.size(); ++t)

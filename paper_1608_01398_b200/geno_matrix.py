@@ -259,6 +259,16 @@ class PackedGenotypeMatrix:
         out._u, out._v = u, v
         return out
 
+    def with_masked_stats(self, keep) -> "PackedGenotypeMatrix":
+        """Same packed bytes standardised with the statistics of the rows with
+        keep != 0 (what subset_rows(rows) would compute), formed on the device;
+        u / v are downloaded only if read."""
+        keep = np.ascontiguousarray(keep, dtype=np.uint8)
+        if keep.shape != (self.n,):
+            raise ValueError("row mask must have one entry per sample")
+        h = _new_handle(lib().gi_matrix_with_masked_stats, self._h.raw, ptr(keep))
+        return PackedGenotypeMatrix(h, self.n, self.p, self.device)
+
     def masked_stats(self, keep) -> tuple[np.ndarray, np.ndarray]:
         """u, v over the rows with keep != 0 -- what subset_rows(rows) would
         compute, without materialising the subset."""

@@ -242,3 +242,43 @@ def test_cli_bench_dense_mode_gives_rel_to_dense(tmp_path):
     for mode, k, support in models:
         by_mode.setdefault(mode, []).append((k, support))
     assert by_mode["gpu"] == by_mode["dense"]
+
+
+@pytest.mark.parametrize("cov", [False, True])
+def test_fold_stats_on_device_and_heldout_scoring(cov):
+    """A CV fold in train mode: the device-formed fold statistics equal the
+    re-packed training rows' (reference subset_rows, geno_matrix.py:305-308),
+    bit for bit; a fit over the row mask that carries the test rows as
+    keep == 2 reports their sum of squared prediction errors, equal to the
+    reference's err @ err through predict (model_select.py:138-139)."""
+    gi = _gi()
+    from paper_1608_01398_b200.iht import last_native_fit_info
+    from paper_1608_01398_b200.model_select import FoldGenotypes, predict
+
+    n, p = 900, 1500
+    codes = oracle.random_codes(n, p, seed=41, missing_rate=0.02)
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    rng = np.random.default_rng(9)
+    test = np.sort(rng.choice(n, 200, replace=False))
+    train = np.setdiff1d(np.arange(n), test)
+    keep = np.zeros(n, np.uint8)
+    keep[train] = 1
+    fold = m.with_masked_stats(keep)
+    sub = m.subset_rows(train)
+    np.testing.assert_array_equal(fold.u, sub.u)
+    np.testing.assert_array_equal(fold.v, sub.v)
+    block = gi.CovariateBlock.build(rng.standard_normal((n, 2)) if cov else None, n=n)
+    cov_tr, cov_te = block.subset_rows(train), block.subset_rows(test)
+    v_tr = gi.StandardizedView(FoldGenotypes(fold, train), cov_tr)
+    v_te = gi.StandardizedView(FoldGenotypes(fold, test), cov_te)
+    support = np.sort(rng.choice(p, 5, replace=False))
+    y = m.ax_columns(support, rng.standard_normal(5)) + rng.normal(0, 0.5, n)
+    res = gi.fit(v_tr, y[train], gi.IhtConfig(k=7),
+                 _heldout=(test, y[test], cov_te.values))
+    info = last_native_fit_info()
+    assert info["heldout_n"] == test.size
+    err = y[test] - predict(v_te, res.model)
+    np.testing.assert_allclose(info["heldout_sse"], float(err @ err), rtol=1e-12)
+    plain = gi.fit(v_tr, y[train], gi.IhtConfig(k=7))  # scoring does not touch the fit
+    np.testing.assert_array_equal(plain.model.weights, res.model.weights)
+    assert last_native_fit_info()["heldout_sse"] is None
