@@ -772,9 +772,17 @@ def main():
     # X^T r streams the base-3 copy (1.6 bits per genotype) when the matrix has
     # no missing genotypes, else the 2-bit BED tiles: algorithmic bytes are
     # those of the format it reads (packed X + r + u, v, s1/cnt + g)
-    base3 = (geno.local if sharded else geno).xtr_base3
-    fmt = "base-3" if base3 else "2-bit"
-    x_bytes = p_local * ((n + 4) // 5) if base3 else p_local * nb
+    geno_l = geno.local if sharded else geno
+    base3 = geno_l.xtr_base3
+    # with missing genotypes the base-3 sweep comes with the missing-genotype
+    # list (2 B per missing genotype + 8 B per 4 KiB block; csrc/missing.cu)
+    mlist = base3 and geno_l.xtr_missing_list
+    fmt = "base-3+missing-list" if mlist else ("base-3" if base3 else "2-bit")
+    list_bytes = 0
+    if mlist:
+        list_bytes = 2 * int(np.sum(geno_l.missing_counts, dtype=np.int64)) + \
+            8 * (((n + 511) // 512) * ((p_local + 31) // 32) + 1)
+    x_bytes = (p_local * ((n + 4) // 5) + list_bytes) if base3 else p_local * nb
     alg_bytes = x_bytes + 8 * n + 24 * p_local
     achieved = alg_bytes / (aty_avg / 1e3) / 1e9
     peak, peak_kind = measured_peak()
@@ -813,17 +821,20 @@ def main():
         "xtr_packed_gbs": p_local * nb / (aty_avg / 1e3) / 1e9,
         "xtr_packed_gbs_all_gpus": a.p * nb / (aty_avg / 1e3) / 1e9,
         "xtr_ms": aty_avg,
-        "xtr_format": ("base-3 device copy, 5 genotypes per byte (no missing genotypes)"
+        "xtr_format": ("base-3 device copy, 5 genotypes per byte (missing as dose 0) + "
+                       f"missing-genotype list ({list_bytes / 1e9:.2f} GB)" if mlist else
+                       "base-3 device copy, 5 genotypes per byte (no missing genotypes)"
                        if base3 else "2-bit BED tiles"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "aty_fast_kernel", "bytes_per_launch": alg_bytes,
+                     "kernel": ("missum_kernel + aty_fast_kernel (one X^T r)" if mlist
+                                else "aty_fast_kernel"), "bytes_per_launch": alg_bytes,
                      "timing": f"CUDA events around each launch on the fit stream, "
                                f"separate instrumented pass of {n_prof} fits",
                      "smem": smem_roofline(n, p_local, aty_avg, clk.get("sm_mhz"),
                                            torch.cuda.get_device_properties(local)
                                            .multi_processor_count, a.missing,
-                                           miss_frac, base3)},
+                                           0.0 if mlist else miss_frac, base3)},
         "parity": parity,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": h2d,

@@ -73,10 +73,12 @@ int gi_matrix_free(gi_matrix *h);
 
 /* ------------------------------------------------------------ inspection */
 int gi_matrix_shape(const gi_matrix *h, int64_t *n, int64_t *p, int *device);
-/* No reference counterpart (device layout): X^T r of a matrix without missing
- * genotypes streams a base-3 copy (5 genotypes per byte, 1.6 bits) built at
- * finalize.  set = -1 queries, 0 drops the copy, 1 builds it when possible;
- * *base3 (may be NULL) receives 1 if the copy exists.  Changing the format
+/* No reference counterpart (device layout): X^T r streams a base-3 copy (5
+ * genotypes per byte, 1.6 bits) built at finalize -- for a matrix with missing
+ * genotypes (at most 5% of them) together with a list of their positions
+ * (2 B each) that supplies the missing sums.  set = -1 queries, 0 drops the
+ * copy, 1 builds it when possible; *base3 (may be NULL) receives 0 (2-bit
+ * tiles), 1 (base-3 copy) or 2 (base-3 copy + missing-genotype list).  Changing the format
  * must not overlap a fit or X^T r on the same handle (it frees or replaces
  * the copy); with_stats copies made earlier keep the copy they share. */
 int gi_matrix_xtr_format(gi_matrix *h, int set, int *base3);
@@ -223,7 +225,8 @@ typedef struct {
   int64_t heldout_n;     /* out: their count */
   int xtr_kernel;        /* out: X^T r kernel the loop ran: 0 exact fp64, 1 fast over the
                             2-bit tiles, 2 fast over the base-3 copy, 3 the lock-step
-                            group's tensor-core sweeps (gi_fit_batched) */
+                            group's tensor-core sweeps (gi_fit_batched), 4 fast over
+                            the base-3 copy plus the missing-genotype list */
 } gi_fit_result;
 
 /* Replaces genoiht.fit (iht.py:326-354) on one GPU: the complete IHT loop with

@@ -114,6 +114,9 @@ struct FastArgs {
   PubArgs pub;
   unsigned int* pub_ticket;
   unsigned long long* pub_out;
+  // base-3 copy of a matrix with missing genotypes: out[j] holds m_j (from
+  // missum_kernel, missing.cu) when the epilogue reads it
+  bool miss_in_out;
 };
 
 __device__ __forceinline__ float dose_term(int code, float r) {
@@ -535,7 +538,9 @@ __global__ void __launch_bounds__(kThreads, 1) aty_fast_kernel(FastArgs a) {
       if (j < m.p) {
         const double uj = a.u[j];
         const double off = (double)a.s1cnt[2 * j] - uj * (double)a.s1cnt[2 * j + 1];
-        const double val = a.v[j] * ((acc[gl * 32 + lane] - uj * srt) + mean * off);
+        double t = acc[gl * 32 + lane];
+        if (a.miss_in_out) t += uj * a.out[j];  // + u_j m_j, as the 2-bit kernel per tile
+        const double val = a.v[j] * ((t - uj * srt) + mean * off);
         a.out[j] = a.scale * val;
         local_max = fmax(local_max, fabs(val));
       }
@@ -661,6 +666,8 @@ int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const flo
   a.scale = scale;
   a.out = out;
   a.gmax = reinterpret_cast<unsigned long long*>(d_gmax);
+  a.miss_in_out = m.x3 != nullptr && m.mlist != nullptr;
+  if (a.miss_in_out && launch_missum(m, rt, out, num_sms, s) != 0) return -1;
   if (pub && pub_ticket && pub_out) {
     a.pub = *pub;
     a.pub_ticket = pub_ticket;

@@ -50,31 +50,76 @@ static int matrix_shell(int64_t n, int64_t p, int device, gi_matrix** out,
 }
 
 // The base-3 copy X^T r streams instead of the 2-bit tiles: 1.6 instead of 2
-// bits per genotype, so 20% fewer HBM bytes and table lookups per sweep.  Only
-// for matrices without missing genotypes (3 states per genotype), and only
-// when it leaves 1/8 of the device memory free; GI_BASE3=0 disables it.
+// bits per genotype, so 20% fewer HBM bytes and table lookups per sweep.  A
+// matrix with missing genotypes gets it too when they are at most 5% of the
+// genotypes: the base-3 copy holds them as dose 0 and a list of their
+// positions (missing.cu, 2 B each) supplies the missing sums m_j, which the
+// 2-bit kernel gets from a second table lookup per byte.  Built only when it
+// leaves 1/8 of the device memory free; GI_BASE3=0 disables it, GI_MISSLIST=0
+// keeps matrices with missing genotypes on the 2-bit tiles.
 // want: 0 drop the copy, 1 build it if possible.
 static int set_base3(gi_matrix* h, int want) {
   if (!want) {
     if (h->x3) GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
     h->x3.reset();
+    h->mlist.reset();
+    h->mofs.reset();
     h->T3 = 0;
     return 0;
   }
   if (h->x3 || h->n == 0 || h->p == 0) return 0;
-  std::vector<uint8_t> flags((size_t)h->G);
-  GI_CUDA_TRY(cudaMemcpy(flags.data(), h->gmiss->ptr, (size_t)h->G, cudaMemcpyDeviceToHost));
-  for (uint8_t f : flags)
-    if (f) return 0;
+  std::vector<int32_t> miss((size_t)h->p);
+  GI_CUDA_TRY(cudaMemcpy(miss.data(), h->miss_cnt->ptr, sizeof(int32_t) * h->p,
+                         cudaMemcpyDeviceToHost));
+  int64_t total = 0;
+  for (int32_t c : miss) total += c;
+  if (total > 0) {
+    const char* env = getenv("GI_MISSLIST");
+    if ((env && env[0] == '0') || (double)total > 0.05 * (double)h->n * (double)h->p) return 0;
+  }
   const int64_t T3 = gi::tiles3_of(h->n);
-  const size_t bytes = (size_t)(T3 * h->G) * GI_BLOCK_BYTES;
+  const int64_t nblk = h->T * h->G;
+  const size_t bytes3 = (size_t)(T3 * h->G) * GI_BLOCK_BYTES;
+  const size_t list_bytes = total > 0 ? (size_t)total * 2 + (size_t)(nblk + 1) * 8 : 0;
   size_t free_b = 0, total_b = 0;
   GI_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-  if (bytes + total_b / 8 > free_b) return 0;
-  std::shared_ptr<DevMem> x3;
-  TRY(alloc(x3, bytes, h->device, false));
+  // the list build also needs nblk + 1 counts and the scan's scratch
+  if (bytes3 + 2 * list_bytes + total_b / 8 > free_b) return 0;
+  std::shared_ptr<DevMem> x3, mlist, mofs;
+  if (total > 0) {
+    gi::MatrixDesc d = h->desc();
+    std::shared_ptr<DevMem> cnt, tmp;
+    TRY(alloc(cnt, (size_t)(nblk + 1) * 8, h->device, true));
+    // + 16 B: staged offset ranges end on a 16-byte boundary
+    TRY(alloc(mofs, (size_t)(nblk + 1) * 8 + 16, h->device, false));
+    // + 16 B: the staged copies round the entry range up to 16-byte units
+    TRY(alloc(mlist, (size_t)total * 2 + 16, h->device, false));
+    TRY(gi::missing_list_count(d, static_cast<int64_t*>(cnt->ptr), h->stream));
+    size_t tmp_bytes = 0;
+    TRY(gi::missing_list_scan(static_cast<int64_t*>(cnt->ptr), static_cast<int64_t*>(mofs->ptr),
+                              nblk, nullptr, tmp_bytes, h->stream));
+    TRY(alloc(tmp, tmp_bytes + 16, h->device, false));
+    TRY(gi::missing_list_scan(static_cast<int64_t*>(cnt->ptr), static_cast<int64_t*>(mofs->ptr),
+                              nblk, tmp->ptr, tmp_bytes, h->stream));
+    int64_t got = 0;
+    GI_CUDA_TRY(cudaMemcpyAsync(&got, static_cast<int64_t*>(mofs->ptr) + nblk, 8,
+                                cudaMemcpyDeviceToHost, h->stream));
+    GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (got != total) {
+      gi_set_error("internal: missing-genotype list holds %lld entries, counts say %lld",
+                   (long long)got, (long long)total);
+      return -1;
+    }
+    TRY(gi::missing_list_fill(d, static_cast<int64_t*>(mofs->ptr),
+                              static_cast<uint16_t*>(mlist->ptr), h->stream));
+    GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  TRY(alloc(x3, bytes3, h->device, false));
   h->x3 = x3;
   h->T3 = T3;
+  h->mlist = mlist;
+  h->mofs = mofs;
+  h->mtotal = total;
   TRY(gi::launch_pack3(h->desc(), static_cast<uint8_t*>(x3->ptr), h->stream));
   GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
@@ -209,6 +254,9 @@ int gi_matrix_with_stats(const gi_matrix* src, const double* u, const double* v,
   h->x = src->x;
   h->x3 = src->x3;
   h->T3 = src->T3;
+  h->mlist = src->mlist;
+  h->mofs = src->mofs;
+  h->mtotal = src->mtotal;
   h->miss_cnt = src->miss_cnt;
   h->gmiss = src->gmiss;
   h->s1cnt = src->s1cnt;
@@ -260,7 +308,7 @@ int gi_matrix_xtr_format(gi_matrix* h, int set, int* base3) {
     DeviceGuard g(h->device);
     TRY(set_base3(h, set));
   }
-  if (base3) *base3 = h->x3 ? 1 : 0;
+  if (base3) *base3 = h->x3 ? (h->mlist ? 2 : 1) : 0;
   return 0;
 }
 
@@ -365,6 +413,9 @@ int gi_matrix_with_masked_stats(const gi_matrix* srcc, const uint8_t* keep, gi_m
   h->x = src->x;
   h->x3 = src->x3;
   h->T3 = src->T3;
+  h->mlist = src->mlist;
+  h->mofs = src->mofs;
+  h->mtotal = src->mtotal;
   h->miss_cnt = src->miss_cnt;
   h->gmiss = src->gmiss;
   h->s1cnt = src->s1cnt;

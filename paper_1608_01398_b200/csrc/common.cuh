@@ -54,6 +54,12 @@ struct MatrixDesc {
   int64_t G;          // SNP groups = ceil(p / 32)
   const uint8_t* x3 = nullptr;  // optional base-3 tiles (read only by X^T r)
   int64_t T3 = 0;               // base-3 sample tiles = ceil(n / 640)
+  // with x3 on a matrix with missing genotypes: the missing positions per
+  // 4 KiB block, (lane << 9) | sample offset, and each block's first entry
+  // (T G + 1 offsets; missing.cu)
+  const uint16_t* mlist = nullptr;
+  const int64_t* mofs = nullptr;
+  int64_t mtotal = 0;  // entries
 };
 
 __host__ __device__ inline int64_t tiles3_of(int64_t n) {
@@ -179,6 +185,14 @@ int launch_subset_rows(const MatrixDesc& src, const MatrixDesc& dst, uint8_t* x,
 int launch_stats(const MatrixDesc& m, const uint32_t* d_rowmask, double* u, double* v,
                  int32_t* d_missing_cnt, int32_t* d_s1cnt, cudaStream_t s);
 int launch_pack3(const MatrixDesc& m, uint8_t* x3, cudaStream_t s);
+// missing-genotype lists (missing.cu): per-block counts (T G + 1 slots, the
+// last left zero), their exclusive scan (tmp == nullptr: size query), the
+// entries; and the per-SNP missing sums m_j = sum rt over the missing samples
+int missing_list_count(const MatrixDesc& m, int64_t* d_cnt, cudaStream_t s);
+int missing_list_scan(const int64_t* d_cnt, int64_t* d_ofs, int64_t nblk, void* tmp,
+                      size_t& tmp_bytes, cudaStream_t s);
+int missing_list_fill(const MatrixDesc& m, const int64_t* d_ofs, uint16_t* d_ent, cudaStream_t s);
+int launch_missum(const MatrixDesc& m, const float* rt, double* out, int num_sms, cudaStream_t s);
 int launch_group_flags(const MatrixDesc& m, const int32_t* d_missing_cnt, uint8_t* flags,
                        cudaStream_t s);
 int launch_aty_fast(const MatrixDesc& m, const uint8_t* group_missing, const float* rt,

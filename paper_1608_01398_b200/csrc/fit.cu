@@ -1056,7 +1056,10 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
             (long long)iterations, F.syncs, F.sync_us, F.launches,
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start)
                 .count());
-  res->xtr_kernel = F.exact_ ? 0 : (F.batch_ ? 3 : (h->desc().x3 != nullptr ? 2 : 1));
+  res->xtr_kernel = F.exact_ ? 0
+                     : F.batch_ ? 3
+                     : h->desc().x3 == nullptr ? 1
+                     : h->desc().mlist != nullptr ? 4 : 2;
   res->kernel_launches = F.launches;
   res->aty_ms_total = F.aty_ms;
   res->aty_launches = F.aty_launches;

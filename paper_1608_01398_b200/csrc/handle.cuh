@@ -132,6 +132,8 @@ struct gi_matrix {
   std::shared_ptr<DevMem> x;         // swizzled tiles (shared by with_stats copies)
   std::shared_ptr<DevMem> x3;        // optional base-3 copy for X^T r (shared likewise)
   int64_t T3 = 0;
+  std::shared_ptr<DevMem> mlist, mofs;  // missing-genotype lists beside x3 (missing.cu)
+  int64_t mtotal = 0;                   // their entries
   std::shared_ptr<DevMem> miss_cnt;  // int32[p]
   std::shared_ptr<DevMem> gmiss;     // uint8[G]
   std::shared_ptr<DevMem> s1cnt;     // int32[2p]: sum of dosages, observed count (all rows)
@@ -160,6 +162,9 @@ struct gi_matrix {
     d.G = G;
     d.x3 = x3 ? static_cast<const uint8_t*>(x3->ptr) : nullptr;
     d.T3 = x3 ? T3 : 0;
+    d.mlist = x3 && mlist ? static_cast<const uint16_t*>(mlist->ptr) : nullptr;
+    d.mofs = x3 && mofs ? static_cast<const int64_t*>(mofs->ptr) : nullptr;
+    d.mtotal = d.mlist ? mtotal : 0;
     return d;
   }
   double* du() const { return static_cast<double*>(u->ptr); }

@@ -216,10 +216,19 @@ class PackedGenotypeMatrix:
     @property
     def xtr_base3(self) -> bool:
         """True when X^T r streams the device's base-3 copy (5 genotypes per
-        byte; built for matrices without missing genotypes, csrc/layout.cu)."""
+        byte, csrc/layout.cu; with missing genotypes, beside their position
+        list, csrc/missing.cu)."""
         out = ctypes.c_int(0)
         check(lib().gi_matrix_xtr_format(self._h.raw, -1, ctypes.byref(out)))
         return bool(out.value)
+
+    @property
+    def xtr_missing_list(self) -> bool:
+        """True when X^T r takes the missing sums from the missing-genotype
+        list (a matrix with missing genotypes on the base-3 copy)."""
+        out = ctypes.c_int(0)
+        check(lib().gi_matrix_xtr_format(self._h.raw, -1, ctypes.byref(out)))
+        return out.value == 2
 
     def set_xtr_base3(self, enable: bool) -> bool:
         """Build (when possible) or drop the base-3 copy; returns xtr_base3.

@@ -210,8 +210,8 @@ def test_aty_batched_fold_residuals_with_fold_stats():
         dev.aty_batched(R, U)
 
 
-@pytest.mark.parametrize("miss", [0.05, 0.0])  # 0.0: the base-3 copy
-def test_fast_aty_identical_columns_get_identical_gradients(miss):
+@pytest.mark.parametrize("miss,misslist", [(0.05, "0"), (0.02, "1"), (0.0, "1")])
+def test_fast_aty_identical_columns_get_identical_gradients(miss, misslist, monkeypatch):
     """SNPs in perfect LD have identical columns; the reference gives them
     identical gradients, so top-k ties go to the lower index.  The fast kernel
     sums its table entries in an order fixed by the word positions (pairwise
@@ -223,8 +223,10 @@ def test_fast_aty_identical_columns_get_identical_gradients(miss):
     base = oracle.random_codes(n, half, seed=17, missing_rate=miss)
     perm = rng.permutation(half)
     codes = np.concatenate([base, base[:, perm]], axis=1)  # column half + i == column perm[i]
+    monkeypatch.setenv("GI_MISSLIST", misslist)  # "0": 2-bit tiles with missing genotypes
     dev = gi.PackedGenotypeMatrix.from_codes(codes)
-    assert dev.xtr_base3 == (miss == 0.0)
+    assert dev.xtr_base3 == (misslist == "1")
+    assert dev.xtr_missing_list == (miss > 0 and misslist == "1")
     for _ in range(3):
         g = dev.aty_genetic(rng.standard_normal(n), mode="fast")
         np.testing.assert_array_equal(g[half:], g[perm])
@@ -264,14 +266,25 @@ def test_base3_copy_xtr(n, p):
     np.testing.assert_array_equal(dev.aty_genetic(r), want)  # exact kernel: 2-bit tiles
 
 
-def test_base3_copy_needs_missing_free_matrix():
+def test_base3_copy_with_missing_genotypes_carries_the_list(monkeypatch):
+    """One missing genotype: the base-3 copy comes with the missing-genotype
+    list (csrc/missing.cu); GI_MISSLIST=0 keeps such a matrix on the 2-bit
+    tiles; a fold copy without that row has a plain base-3 copy."""
     codes = oracle.random_codes(700, 90, seed=5, missing_rate=0.0)
     codes[13, 77] = 1  # one missing genotype
     dev = _gm().PackedGenotypeMatrix.from_codes(codes)
-    assert not dev.xtr_base3
-    assert dev.set_xtr_base3(True) is False
+    assert dev.xtr_base3 and dev.xtr_missing_list
     sub = dev.subset_rows(np.array([i for i in range(700) if i != 13]))
-    assert sub.xtr_base3  # the fold copy without that row has none
+    assert sub.xtr_base3 and not sub.xtr_missing_list
+    monkeypatch.setenv("GI_MISSLIST", "0")
+    dev0 = _gm().PackedGenotypeMatrix.from_codes(codes)
+    assert not dev0.xtr_base3
+    assert dev0.set_xtr_base3(True) is False
+    r = np.random.default_rng(3).standard_normal(700)
+    want = oracle.OraclePacked.from_codes(codes).aty_genetic(r)
+    scale = np.sqrt(np.mean(want ** 2))
+    for m in (dev, dev0):
+        assert np.max(np.abs(m.aty_genetic(r, mode="fast") - want)) <= 2e-6 * scale + 1e-12
 
 
 def test_base3_copy_env_switch(monkeypatch):
@@ -288,3 +301,42 @@ def test_base3_copy_env_switch(monkeypatch):
     scale = np.sqrt(np.mean(want ** 2))
     for m in (dev, dev2):
         assert np.max(np.abs(m.aty_genetic(r, mode="fast") - want)) <= 2e-6 * scale + 1e-12
+
+
+@pytest.mark.parametrize("n,p,miss", [(1, 1, 0.5), (5, 33, 0.04), (511, 31, 0.03), (512, 32, 0.02),
+                                      (641, 65, 0.02), (1281, 700, 0.01), (5000, 3000, 0.02),
+                                      (20000, 257, 0.03), (3000, 8000, 0.001)])
+def test_missing_list_xtr(n, p, miss):
+    """X^T r of a matrix with missing genotypes over the base-3 copy plus the
+    missing-genotype list (csrc/missing.cu): within the fast kernel's
+    tolerance of the reference, close to the 2-bit tiles' sweep, and the same
+    bits on every call (the list sums are exact integers)."""
+    rng = np.random.default_rng(n * 13 + p)
+    codes = oracle.random_codes(n, p, seed=n + 3 * p, missing_rate=miss)
+    codes[n - 1, p - 1] = 1  # the last sample of the last SNP
+    codes[:, 0] = 1  # an all-missing column
+    if p > 2:
+        codes[: n // 2, 1] = 1
+    ref = oracle.OraclePacked.from_codes(codes)
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    rate = float(np.mean(codes == 1))
+    assert dev.xtr_missing_list == (rate <= 0.05)
+    for shift in (0.0, 1.5, -40.0):
+        r = rng.standard_normal(n) + shift
+        want = ref.aty_genetic(r)
+        scale = max(np.sqrt(np.mean(want ** 2)), 1e-300)
+        got = dev.aty_genetic(r, mode="fast")
+        assert np.max(np.abs(got - want)) <= 2e-6 * scale + 1e-12
+        np.testing.assert_array_equal(dev.aty_genetic(r, mode="fast"), got)
+    if dev.xtr_missing_list:
+        dev.set_xtr_base3(False)  # the 2-bit tiles' lookup-table sweep
+        g2 = dev.aty_genetic(r, mode="fast")
+        assert np.max(np.abs(g2 - got)) <= 2e-6 * scale + 1e-12
+        assert dev.set_xtr_base3(True) and dev.xtr_missing_list
+        np.testing.assert_array_equal(dev.aty_genetic(r, mode="fast"), got)
+
+
+def test_missing_list_above_five_percent_stays_on_2bit_tiles():
+    codes = oracle.random_codes(2000, 300, seed=2, missing_rate=0.08)
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    assert not dev.xtr_base3 and not dev.xtr_missing_list

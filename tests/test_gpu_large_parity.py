@@ -3,9 +3,9 @@
 The golden fits and CV runs in tests/golden/large.npz (tools/make_golden.py,
 produced by genoiht 0.1.0 itself) are big enough that the native loop runs
 the lookup-table X^T r kernel, not the exact fp64 one (more than 2 MiB of
-tiles and n > 8 (k + c + 1); csrc/fit.cu NativeFit): over the 2-bit tiles
-with the missing-sum lookups when genotypes are missing (2-3%), over the
-base-3 copy otherwise.  The matrices are rebuilt on the device by the
+tiles and n > 8 (k + c + 1); csrc/fit.cu NativeFit): over the base-3 copy,
+with the missing-genotype list when genotypes are missing (2-3%), and for
+those also over the 2-bit tiles with the missing-sum lookups.  The matrices are rebuilt on the device by the
 generator whose CPU twin made the reference's bytes (checked by SHA-256).
 
 Bar (north star): support, iteration count and reason identical; beta, b_cov
@@ -41,18 +41,25 @@ def _matrix(case):
     return m
 
 
-@pytest.mark.parametrize("name", FITS)
-def test_large_fit_matches_reference(name):
+FIT_CASES = [(k, "1") for k in FITS] + [(k, "0") for k in FITS if LARGE[k]["missing"] > 0]
+
+
+@pytest.mark.parametrize("name,misslist", FIT_CASES)
+def test_large_fit_matches_reference(name, misslist, monkeypatch):
+    """Missing genotypes: X^T r over the base-3 copy plus the missing list
+    (GI_MISSLIST=1, the default) and over the 2-bit tiles (=0)."""
     import paper_1608_01398_b200 as gi
     from paper_1608_01398_b200.iht import last_native_fit_info
 
+    monkeypatch.setenv("GI_MISSLIST", misslist)
     case = LARGE[name]
     m = _matrix(case)
     raw = case["covar_raw"]
     block = gi.CovariateBlock.build(raw if raw.size else None, n=case["n"])
     res = gi.fit(gi.StandardizedView(m, block), case["y"], gi.IhtConfig(k=int(case["k"])))
     info = last_native_fit_info()
-    want_kernel = "fast-2bit" if case["missing"] > 0 else "fast-base3"
+    want_kernel = "fast-base3" if case["missing"] == 0 else \
+        ("fast-base3-misslist" if misslist == "1" else "fast-2bit")
     assert info["xtr_kernel"] == want_kernel, info
     np.testing.assert_array_equal(res.model.support, case["support"])
     assert res.iterations == case["iterations"] and res.reason == case["reason"]
