@@ -12,7 +12,7 @@
 //
 //   list    per 4 KiB block (tile t of 512 samples, group g of 32 SNPs), one
 //           uint16 per missing genotype: (SNP lane << 9) | sample offset,
-//           in (word, lane, sample) order; ofs[t G + g] = first entry of the
+//           round-robin over the lanes within windows of 32 samples; ofs[t G + g] = first entry of the
 //           block (int64, T G + 1 entries).  At 2% missing that is 0.04 B per
 //           genotype next to the base-3 stream's 0.2 (2-bit tiles: 0.25).
 //   missum  one CTA per chunk of groups walks every tile in order: the tile's
@@ -35,6 +35,8 @@
 // point as two 21-bit halves cost a second atomic and an 8-byte read per
 // entry: 10.1 ms for config 5's 5.1e9 entries, 14 shared-memory wavefronts
 // per 32 entries.)
+#include <stdlib.h>
+
 #include <algorithm>
 #include <mutex>
 
@@ -68,35 +70,52 @@ __global__ void miss_count_kernel(MatrixDesc m, int64_t* __restrict__ cnt) {
   }
 }
 
-// the entries, one warp per block: for word w = 0..31, lane L takes word w of
-// SNP L (byte ((L ^ w) << 7) + 4 L of the swizzled block) and writes its
-// missing samples 16 w + s in order after the lanes below it
+// the 16 missing flags of a 2-bit word (bit s = sample s)
+__device__ __forceinline__ uint32_t missing_mask16(uint32_t w) {
+  uint32_t x = missing_bits(w);
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  return (x | (x >> 8)) & 0x0000FFFFu;
+}
+
+// the entries, one warp per block, in windows of kWin words (16 kWin
+// samples): lane L gathers the missing flags of SNP L over the window (word w
+// at byte ((L ^ w) << 7) + 4 L of the swizzled block) and the window's entries
+// are written round by round -- every lane's first missing sample, then every
+// lane's second, ... -- so consecutive entries tend to name different SNPs
+// (fewer colliding shared-memory atomics in missum_kernel) and nearby samples
+// (fewer bank conflicts on the residual reads)
+template <int kWin>
 __global__ void miss_fill_kernel(MatrixDesc m, const int64_t* __restrict__ ofs,
                                  uint16_t* __restrict__ ent) {
   const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
   const int64_t nblk = m.T * m.G;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t b = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); b < nblk;
        b += warps) {
     const uint8_t* blk = m.x + b * GI_BLOCK_BYTES;
     int64_t pos = ofs[b];
-    for (int w = 0; w < 32; ++w) {
-      uint32_t mb = missing_bits(*reinterpret_cast<const uint32_t*>(blk + ((lane ^ w) << 7) +
-                                                                    (lane << 2)));
-      const int c = __popc(mb);
-      int incl = c;
+    for (int w0 = 0; w0 < 32; w0 += kWin) {
+      uint64_t mk = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+      for (int k = 0; k < kWin; ++k) {
+        const int w = w0 + k;
+        mk |= (uint64_t)missing_mask16(
+                  *reinterpret_cast<const uint32_t*>(blk + ((lane ^ w) << 7) + (lane << 2)))
+              << (16 * k);
       }
-      int64_t at = pos + (incl - c);
-      while (mb) {
-        const int s = __ffs(mb) >> 1;  // field index of the lowest set bit (bit 2s)
-        mb &= mb - 1u;
-        ent[at++] = (uint16_t)((lane << 9) | (16 * w + s));
+      while (true) {
+        const uint32_t act = __ballot_sync(0xffffffffu, mk != 0);
+        if (!act) break;
+        if (mk) {
+          const int bit = __ffsll((long long)mk) - 1;
+          mk &= mk - 1;
+          ent[pos + __popc(act & lt)] = (uint16_t)((lane << 9) | (16 * w0 + bit));
+        }
+        pos += __popc(act);
       }
-      pos += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
 }
@@ -321,7 +340,17 @@ int missing_list_fill(const MatrixDesc& m, const int64_t* d_ofs, uint16_t* d_ent
   if (nblk == 0) return 0;
   int64_t grid = (nblk + 7) / 8;
   if (grid > 148 * 16) grid = 148 * 16;
-  miss_fill_kernel<<<(unsigned)grid, 256, 0, s>>>(m, d_ofs, d_ent);
+  static const int win = [] {
+    const char* e = getenv("GI_MISS_WIN");
+    const int w = e ? atoi(e) : 2;
+    return w == 1 || w == 2 || w == 4 ? w : 2;
+  }();
+  if (win == 1)
+    miss_fill_kernel<1><<<(unsigned)grid, 256, 0, s>>>(m, d_ofs, d_ent);
+  else if (win == 4)
+    miss_fill_kernel<4><<<(unsigned)grid, 256, 0, s>>>(m, d_ofs, d_ent);
+  else
+    miss_fill_kernel<2><<<(unsigned)grid, 256, 0, s>>>(m, d_ofs, d_ent);
   GI_LAUNCH_CHECK();
   return 0;
 }
