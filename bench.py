@@ -634,8 +634,9 @@ def main():
     if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(a))
     if os.environ.get("GI_BENCH_PROBE_RANKS") == "1":  # tests: the rank launch alone
-        print(json.dumps({"probe_rank": int(os.environ.get("RANK", "0")), "world": world,
-                          "master_addr": os.environ.get("MASTER_ADDR")}), flush=True)
+        line = json.dumps({"probe_rank": int(os.environ.get("RANK", "0")), "world": world,
+                           "master_addr": os.environ.get("MASTER_ADDR")}) + "\n"
+        os.write(1, line.encode())  # one write: the ranks share the pipe
         return
     if a.workload not in ("c3", "c5"):
         secondary(a)

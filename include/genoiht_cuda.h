@@ -267,6 +267,35 @@ int gi_fit_batched(gi_matrix *h, gi_batch *batch, const double *y, const double 
                    const gi_fit_config *cfg, const int64_t *warm_idx, const double *warm_w,
                    int64_t warm_k, const double *bcov0, gi_fit_result *res);
 
+/* Many fits in one call (no reference counterpart: cv_iht's fold x budget
+ * loop, model_select.py:124-139, and a model-size path, cli.py:326-331, run
+ * their fits one after another): job i is gi_fit (batch == NULL) or
+ * gi_fit_batched (batch != NULL) with job i's arguments, run on `threads`
+ * native worker threads that take the jobs in index order.  Each job's
+ * status (0 or a gi_fit error code) and error message land in the job; the
+ * call returns 0 when every job succeeded, -1 otherwise.  Host threads of
+ * the caller's language (and its interpreter lock) stay out of the fits'
+ * start-up: a Python thread pool needed ~1 ms per job to hand 32 fits their
+ * threads. */
+typedef struct gi_fit_job {
+  gi_matrix *h;
+  const double *y;
+  const double *C;
+  int64_t c;
+  const uint8_t *keep;
+  const double *u;
+  const double *v;
+  const gi_fit_config *cfg;
+  const int64_t *warm_idx;
+  const double *warm_w;
+  int64_t warm_k;
+  const double *bcov0;
+  gi_fit_result *res;
+  int status;       /* out */
+  char error[256];  /* out: gi_last_error() of a failed job */
+} gi_fit_job;
+int gi_fit_many(gi_batch *batch, gi_fit_job *jobs, int64_t njobs, int threads);
+
 /* ------------------------------------------------ SNP-sharded native loop */
 /* One process per GPU, each holding a contiguous SNP block [j_base, j_base +
  * p_local) of the matrix.  The shards exchange only the

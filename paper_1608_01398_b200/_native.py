@@ -51,6 +51,16 @@ class FitOut(ctypes.Structure):
                 ("xtr_kernel", c_int)]
 
 
+class FitJob(ctypes.Structure):
+    """gi_fit_job: one fit of gi_fit_many."""
+
+    _fields_ = [("h", c_vp), ("y", c_vp), ("C", c_vp), ("c", c_i64), ("keep", c_vp),
+                ("u", c_vp), ("v", c_vp), ("cfg", ctypes.POINTER(FitConfig)),
+                ("warm_idx", c_vp), ("warm_w", c_vp), ("warm_k", c_i64), ("bcov0", c_vp),
+                ("res", ctypes.POINTER(FitOut)), ("status", c_int),
+                ("error", ctypes.c_char * 256)]
+
+
 def _declare(lib):
     P = c_vp
     sig = {
@@ -104,6 +114,7 @@ def _declare(lib):
         "gi_comm_create_callbacks": ([c_int, c_int, P, P, P, P], c_int),
         "gi_comm_free": ([P], c_int),
         "gi_matrix_with_masked_stats": ([P, P, P], c_int),
+        "gi_fit_many": ([P, P, c_i64, c_int], c_int),
         "gi_batch_create": ([P, c_int, P], c_int),
         "gi_batch_stats": ([P, P, P], c_int),
         "gi_batch_free": ([P], c_int),

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <deque>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/genoiht_cuda.h"
@@ -46,7 +47,10 @@ struct gi_batch {
   int64_t pcap = 0;
   unsigned int* tickets = nullptr;
   int8_t* qimg = nullptr;
-  std::vector<void*> allocs;
+  // from the device's stream-ordered pool (kept mapped): a CV creates and
+  // drops a group, and cudaMalloc / cudaFree of the ~0.3 GB digit image cost
+  // ~15 / ~40 ms at config 4
+  std::vector<std::shared_ptr<DevMem>> allocs;
   cudaEvent_t events[kEvents] = {};
   uint64_t sweeps = 0;
   // group state
@@ -66,7 +70,7 @@ struct gi_batch {
   ~gi_batch() {
     DeviceGuard g(device);
     if (stream) cudaStreamSynchronize(stream);
-    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
     for (cudaEvent_t e : events)
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -203,23 +207,25 @@ int gi_batch_create(gi_matrix* h, int max_rhs, gi_batch** out) {
   if (e != cudaSuccess) return fail(e);
   for (auto& ev : b->events)
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
-  auto dev = [&](size_t bytes, void** p) {
-    cudaError_t r = cudaMalloc(p, bytes);
-    if (r == cudaSuccess) {
-      b->allocs.push_back(*p);
-      r = cudaMemset(*p, 0, bytes);
-    }
-    return r;
+  auto dev = [&](size_t bytes, bool zero, auto** p) {
+    std::shared_ptr<DevMem> m;
+    if (alloc(m, bytes, b->device, zero) != 0) return false;
+    b->allocs.push_back(m);
+    *p = static_cast<std::remove_reference_t<decltype(*p)>>(m->ptr);
+    return true;
   };
   const int mr = b->max_rhs;
   b->pcap = 4 * 148 * (int64_t)mr;
-  if ((e = dev(sizeof(gi::XtrRhs) * mr, reinterpret_cast<void**>(&b->d_desc))) ||
-      (e = dev(sizeof(double) * 2 * mr, reinterpret_cast<void**>(&b->qscal))) ||
-      (e = dev(sizeof(long long) * mr, reinterpret_cast<void**>(&b->qsum))) ||
-      (e = dev(sizeof(double) * b->pcap, reinterpret_cast<void**>(&b->partials))) ||
-      (e = dev(sizeof(unsigned int) * mr, reinterpret_cast<void**>(&b->tickets))) ||
-      (e = dev((size_t)gi::xtr_mma_qimg_bytes(b->desc, mr), reinterpret_cast<void**>(&b->qimg))))
-    return fail(e);
+  // the digit image is written in full by each sweep's quantiser before use
+  if (!dev(sizeof(gi::XtrRhs) * mr, true, &b->d_desc) ||
+      !dev(sizeof(double) * 2 * mr, true, &b->qscal) ||
+      !dev(sizeof(long long) * mr, true, &b->qsum) ||
+      !dev(sizeof(double) * b->pcap, true, &b->partials) ||
+      !dev(sizeof(unsigned int) * mr, true, &b->tickets) ||
+      !dev((size_t)gi::xtr_mma_qimg_bytes(b->desc, mr), false, &b->qimg)) {
+    delete b;
+    return -1;
+  }
   *out = b;
   return 0;
 }

@@ -424,12 +424,15 @@ int gi_matrix_with_masked_stats(const gi_matrix* srcc, const uint8_t* keep, gi_m
   GI_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   TRY(alloc(h->u, sizeof(double) * std::max<int64_t>(h->p, 1), h->device, true));
   TRY(alloc(h->v, sizeof(double) * std::max<int64_t>(h->p, 1), h->device, true));
+  h->fold_keep.resize((size_t)h->n);
+  for (int64_t i = 0; i < h->n; ++i) h->fold_keep[(size_t)i] = keep[i] != 0;
   if (h->p > 0) {
+    TRY(alloc(h->fold_s1cnt, sizeof(int32_t) * 2 * h->p, h->device, false));
     TRY(h->s_a.ensure(mask.size() * 4, h->device));
     GI_CUDA_TRY(cudaMemcpyAsync(h->s_a.mem->ptr, mask.data(), mask.size() * 4,
                                 cudaMemcpyHostToDevice, h->stream));
-    TRY(gi::launch_stats(h->desc(), h->s_a.as<uint32_t>(), h->du(), h->dv(), nullptr, nullptr,
-                         h->stream));
+    TRY(gi::launch_stats(h->desc(), h->s_a.as<uint32_t>(), h->du(), h->dv(), nullptr,
+                         static_cast<int32_t*>(h->fold_s1cnt->ptr), h->stream));
     GI_CUDA_TRY(cudaStreamSynchronize(h->stream));
   }
   *out = h.release();

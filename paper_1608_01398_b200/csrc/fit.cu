@@ -19,7 +19,9 @@
 
 #include <algorithm>
 #include <map>
+#include <atomic>
 #include <mutex>
+#include <thread>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -803,8 +805,14 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
     n_eff = (double)cnt;
     GI_CUDA_TRY(cudaMemcpyAsync(ws->rowmask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice,
                                 s));
-    // per-SNP counts over the kept rows (its u, v outputs are overwritten below)
-    TRY(gi::launch_stats(d, ws->rowmask, ws->u, ws->v, nullptr, ws->s1cnt, s));
+    // per-SNP counts over the kept rows: the fold handle's own when it was made
+    // for exactly these rows (gi_matrix_with_masked_stats; every budget of a
+    // CV fold), else one counting pass (its u, v outputs are overwritten below)
+    if (h->fold_s1cnt && h->fold_keep == fit_rows)
+      GI_CUDA_TRY(cudaMemcpyAsync(ws->s1cnt, h->fold_s1cnt->ptr, sizeof(int32_t) * 2 * p,
+                                  cudaMemcpyDeviceToDevice, s));
+    else
+      TRY(gi::launch_stats(d, ws->rowmask, ws->u, ws->v, nullptr, ws->s1cnt, s));
   } else {
     GI_CUDA_TRY(cudaMemcpyAsync(ws->s1cnt, h->s1cnt->ptr, sizeof(int32_t) * 2 * p,
                                 cudaMemcpyDeviceToDevice, s));
@@ -1081,6 +1089,37 @@ extern "C" int gi_fit_batched(gi_matrix* h, gi_batch* batch, const double* y, co
   CHECK_ARG(batch != nullptr, "NULL batch group");
   return fit_impl(h, nullptr, 0, y, C, c, keep, u, v, cfg, warm_idx, warm_w, warm_k, bcov0, res,
                   batch);
+}
+
+extern "C" int gi_fit_many(gi_batch* batch, gi_fit_job* jobs, int64_t njobs, int threads) {
+  CHECK_ARG(njobs >= 0 && (njobs == 0 || jobs != nullptr), "invalid job list");
+  CHECK_ARG(threads >= 1, "need at least one thread");
+  std::atomic<int64_t> next{0};
+  std::atomic<int> failed{0};
+  auto worker = [&]() {
+    for (int64_t i = next.fetch_add(1); i < njobs; i = next.fetch_add(1)) {
+      gi_fit_job& j = jobs[i];
+      const int rc = fit_impl(j.h, nullptr, 0, j.y, j.C, j.c, j.keep, j.u, j.v, j.cfg, j.warm_idx,
+                              j.warm_w, j.warm_k, j.bcov0, j.res, batch);
+      j.status = rc;
+      j.error[0] = '\0';
+      if (rc != 0) {
+        snprintf(j.error, sizeof(j.error), "%s", gi_last_error());
+        failed.store(1);
+      }
+    }
+  };
+  const int nt = (int)std::min<int64_t>(threads, std::max<int64_t>(njobs, 1));
+  std::vector<std::thread> pool;
+  pool.reserve((size_t)nt);
+  for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  if (failed.load()) {
+    gi_set_error("gi_fit_many: at least one job failed (see the jobs' status)");
+    return -1;
+  }
+  return 0;
 }
 
 extern "C" int gi_fit_sharded(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y,

@@ -137,6 +137,10 @@ struct gi_matrix {
   std::shared_ptr<DevMem> miss_cnt;  // int32[p]
   std::shared_ptr<DevMem> gmiss;     // uint8[G]
   std::shared_ptr<DevMem> s1cnt;     // int32[2p]: sum of dosages, observed count (all rows)
+  // a fold handle (gi_matrix_with_masked_stats): its rows (0/1 per sample) and
+  // the (sum of dosages, observed count) pairs over them
+  std::vector<uint8_t> fold_keep;
+  std::shared_ptr<DevMem> fold_s1cnt;
   std::shared_ptr<DevMem> u, v;      // fp64[p], owned per handle
   cudaStream_t stream = nullptr;
   std::mutex mu;

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--p", type=int, default=500000)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--switch", type=float, default=0.0, help="sys.setswitchinterval (s)")
+    ap.add_argument("--gc-off", action="store_true", help="gc.disable() around the runs")
     a = ap.parse_args()
     import paper_1608_01398_b200 as gi
     from paper_1608_01398_b200 import model_select as ms
@@ -50,6 +51,24 @@ def main():
         setattr(L, fn, wrap("native", getattr(L, fn)))
     if a.switch > 0:
         sys.setswitchinterval(a.switch)
+    if a.gc_off:
+        import gc
+        gc.disable()
+    orig_run = ms._run_concurrently
+
+    def run_concurrently(jobs, workers):
+        t_sub = time.perf_counter()
+
+        def tagged(job):
+            def inner():
+                with lock:
+                    events.append(("job", threading.get_ident(), time.perf_counter(), t_sub))
+                return job()
+            return inner
+        return orig_run([tagged(j) for j in jobs], workers)
+
+    ms._run_concurrently = run_concurrently
+    ms.fit_many = wrap("fit_many", ms.fit_many)
     ms.fit = wrap("fit", orig_fit)
     ms.predict = wrap("predict", orig_pred)
     ms._fold_views = wrap("fold_views", orig_views)
@@ -74,6 +93,10 @@ def main():
             horizon = int(1e3 * max(e for _, e in fits)) + 1
             live = [sum(1 for s, e in fits if s * 1e3 <= t < e * 1e3) for t in range(horizon)]
             print("  live fits per 10 ms:", [max(live[i:i + 10]) for i in range(0, horizon, 10)])
+        jobs = sorted(s for s, _ in by.get("job", []))
+        if jobs:
+            print("  job dequeue ms (sorted, every 4th of the first 40):",
+                  [round(1e3 * j, 1) for j in jobs[:40:4]])
         nat = sorted(by.get("native", []))
         if fits and len(nat) == len(fits):
             pre = [ns - fs for (fs, _), (ns, _) in zip(fits, nat)]
