@@ -282,3 +282,33 @@ def test_fold_stats_on_device_and_heldout_scoring(cov):
     plain = gi.fit(v_tr, y[train], gi.IhtConfig(k=7))  # scoring does not touch the fit
     np.testing.assert_array_equal(plain.model.weights, res.model.weights)
     assert last_native_fit_info()["heldout_sse"] is None
+
+
+def test_fit_many_matches_single_fits_and_reports_per_job_errors():
+    """gi_fit_many (iht.fit_many): several fits in one library call on native
+    threads give the same results as one fit() each; a bad job reports its own
+    error without touching the others."""
+    gi = _gi()
+    from paper_1608_01398_b200.iht import fit_many
+
+    n, p = 1500, 6000
+    codes = oracle.random_codes(n, p, seed=51, missing_rate=0.01)
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=n))
+    rng = np.random.default_rng(4)
+    support = np.sort(rng.choice(p, 6, replace=False))
+    y = m.ax_columns(support, rng.standard_normal(6)) + rng.normal(0, 0.3, n)
+    bad = y.copy()
+    bad[3] = np.nan
+    ks = [2, 5, 9, 14]
+    specs = [(view, y, gi.IhtConfig(k=k), None, None, None) for k in ks]
+    specs.insert(2, (view, bad, gi.IhtConfig(k=3), None, None, None))
+    outs = fit_many(specs, threads=4)
+    assert isinstance(outs[2][1], ValueError) and outs[2][0] is None
+    got = [o for i, o in enumerate(outs) if i != 2]
+    for k, (res, exc, info) in zip(ks, got):
+        assert exc is None and info["xtr_kernel"] != "unknown"
+        want = gi.fit(view, y, gi.IhtConfig(k=k))
+        np.testing.assert_array_equal(res.model.support, want.model.support)
+        np.testing.assert_array_equal(res.model.weights, want.model.weights)
+        assert res.iterations == want.iterations
