@@ -1,6 +1,7 @@
 # Round-2 evidence: GPU suite, smoke, default bench (config 3, parity + CPU
 # baseline), reference arm, config 5 / 2 / 4 lines, the launch list of the
-# default bench command and one ncu --set full of the X^T r kernel.
+# default bench command, one ncu --set full of the X^T r kernel, and the
+# config-5 X^T r pair (missum_kernel + aty_fast_kernel over the base-3 copy).
 cd "$GRAFT_REPO_ROOT"; export PYTHONPATH="$GRAFT_REPO_ROOT"; mkdir -p gpurun_out/ev
 make -s -C oracle >/dev/null 2>&1
 timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/ev/gputest.log 2>&1; echo "tests rc=$?" >> gpurun_out/ev/gputest.log
@@ -16,4 +17,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --c
 echo "list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:aty_fast -s 5 -c 1 -o gpurun_out/ev/prof_c3 $CMD > gpurun_out/ev/ncu_full.log 2>&1
 echo "full rc=$?"
+C5="python bench.py --workload c5 --steps 1 --warmup 3 --no-cpu --no-parity"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum,sm__cycles_elapsed.avg.per_second \
+  --clock-control none -k regex:"missum|aty_fast" -c 2 --csv --log-file gpurun_out/ev/c5_xtr_kernels.csv $C5 > gpurun_out/ev/ncu_c5.log 2>&1
+echo "c5 ncu rc=$?"
 echo done
