@@ -356,7 +356,7 @@ int missing_list_fill(const MatrixDesc& m, const int64_t* d_ofs, uint16_t* d_ent
 }
 
 int launch_missum(const MatrixDesc& m, const float* rt, double* out, int num_sms, cudaStream_t s) {
-  if (m.p == 0 || m.G == 0) return 0;
+  if (m.p == 0 || m.G == 0 || m.T == 0) return 0;
   static std::once_flag once;
   static cudaError_t cfg_err = cudaSuccess;
   std::call_once(once, [] {

@@ -340,3 +340,24 @@ def test_missing_list_above_five_percent_stays_on_2bit_tiles():
     codes = oracle.random_codes(2000, 300, seed=2, missing_rate=0.08)
     dev = _gm().PackedGenotypeMatrix.from_codes(codes)
     assert not dev.xtr_base3 and not dev.xtr_missing_list
+
+
+def test_missing_list_tile_overflow_path():
+    """Missing genotypes concentrated in one sample tile (every SNP missing on
+    the first 512 samples, 2.5% overall): that tile's entries overflow the
+    missing-sum kernel's staging buffer and are read from global memory
+    (csrc/missing.cu), with the same results as the staged tiles."""
+    n, p = 512 * 40, 3000
+    codes = oracle.random_codes(n, p, seed=77, missing_rate=0.0)
+    codes[:512, :] = 1
+    dev = _gm().PackedGenotypeMatrix.from_codes(codes)
+    assert dev.xtr_missing_list
+    ref = oracle.OraclePacked.from_codes(codes)
+    r = np.random.default_rng(8).standard_normal(n) + 0.3
+    want = ref.aty_genetic(r)
+    scale = np.sqrt(np.mean(want ** 2))
+    got = dev.aty_genetic(r, mode="fast")
+    assert np.max(np.abs(got - want)) <= 2e-6 * scale + 1e-12
+    dev.set_xtr_base3(False)
+    g2 = dev.aty_genetic(r, mode="fast")
+    assert np.max(np.abs(g2 - want)) <= 2e-6 * scale + 1e-12
