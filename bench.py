@@ -59,6 +59,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "IHT iterations/sec (X^T r packed-genotype GB/s vs HBM peak)"
 FALLBACK_HBM_GBS = 6650.0
+SPEC_HBM_GBS = 8000.0  # B200 datasheet HBM3e bandwidth ("~8 TB/s", BASELINE.json)
 
 
 def parse():
@@ -828,6 +829,8 @@ def main():
                        if base3 else "2-bit BED tiles"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     # against the B200 datasheet's ~8 TB/s as well (north star)
+                     "spec_peak": SPEC_HBM_GBS, "frac_of_spec": achieved / SPEC_HBM_GBS,
                      "kernel": ("missum_kernel + aty_fast_kernel (one X^T r)" if mlist
                                 else "aty_fast_kernel"), "bytes_per_launch": alg_bytes,
                      "timing": f"CUDA events around each launch on the fit stream, "
