@@ -293,6 +293,21 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
   const uint32_t b_dfull = b_done + 8 * 2 * R;          // [2]
   const uint32_t b_dempty = b_dfull + 8 * 2;            // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 8 * kBlkSlots + 2 * NB + 4 * R + 4);
+  // the right-hand sides' descriptors and quantiser scalars, read by every
+  // epilogue: cached here instead of a dependent global load per use
+  XtrRhs* s_rhs = reinterpret_cast<XtrRhs*>(
+      reinterpret_cast<uint8_t*>(tmem_holder) + 16);
+  double* s_q = reinterpret_cast<double*>(s_rhs + kXtrMaxRhs);  // [rhs]: scale, mean, sum
+  static_assert(C::kBlkBytes + 2 * R * C::kQBytes + 8 * (8 * kBlkSlots + 2 * NB + 4 * R + 4) +
+                        16 + kXtrMaxRhs * (sizeof(XtrRhs) + 3 * sizeof(double)) <=
+                    kSmemMma,
+                "shared memory");
+  for (int q = threadIdx.x; q < a.nrhs; q += blockDim.x) {
+    s_rhs[q] = a.rhs[q];
+    s_q[3 * q] = a.qscal[2 * q];
+    s_q[3 * q + 1] = a.qscal[2 * q + 1];
+    s_q[3 * q + 2] = (double)a.qsum[q];
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
@@ -487,8 +502,32 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
       bar_wait(b_dfull + 8 * sl, mt_done & 1u);
       tc_fence_after();
       const int64_t j = g * 32 + lane;
+      const bool live_j = valid && j < m.p;
+      // per-SNP statistics of the two right-hand sides of an 8-column step,
+      // loaded one step ahead so their global latency overlaps the TMEM reads
+      // and arithmetic of the current step (the epilogue took 18% of a decode
+      // warp's cycles at config 4 with a dependent descriptor load per use)
+      double nu[2] = {0.0, 0.0}, nv[2] = {0.0, 0.0};
+      int ns1[2] = {0, 0}, ncn[2] = {0, 0};
+      auto fetch = [&](int c0n) {
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb) {
+          const int rhs = c0n / 4 + rb;
+          if (rhs < a.nrhs && live_j) {
+            const XtrRhs& rd = s_rhs[rhs];
+            nu[rb] = __ldg(rd.u + j);
+            nv[rb] = __ldg(rd.v + j);
+            ns1[rb] = __ldg(rd.s1cnt + 2 * j);
+            ncn[rb] = __ldg(rd.s1cnt + 2 * j + 1);
+          }
+        }
+      };
+      fetch(0);
 #pragma unroll 1
       for (int c0 = 0; c0 < N; c0 += 8) {
+        const double cu[2] = {nu[0], nu[1]}, cv[2] = {nv[0], nv[1]};
+        const int cs1[2] = {ns1[0], ns1[1]}, ccn[2] = {ncn[0], ncn[1]};
+        if (c0 + 8 < N) fetch(c0 + 8);
         int32_t dd[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
         for (int e = 0; e < ISS; ++e) {
@@ -515,17 +554,16 @@ __global__ void __launch_bounds__(Cfg<N, ISS, MISS>::kThreads, 1) xtr_mma_kernel
         for (int rb = 0; rb < 2; ++rb) {
           const int rhs = c0 / 4 + rb;
           if (rhs < a.nrhs) {  // warp-uniform
-            const XtrRhs rd = a.rhs[rhs];
+            const XtrRhs& rd = s_rhs[rhs];
             double val = 0.0;
-            if (valid && j < m.p) {
+            if (live_j) {
               const long long Tq = (long long)dd[4 * rb] + 128ll * dd[4 * rb + 1] +
                                    16384ll * dd[4 * rb + 2] + 2097152ll * dd[4 * rb + 3];
               const long long Mq = (long long)mm[4 * rb] + 128ll * mm[4 * rb + 1] +
                                    16384ll * mm[4 * rb + 2] + 2097152ll * mm[4 * rb + 3];
-              const double sc = a.qscal[2 * rhs], mean = a.qscal[2 * rhs + 1];
-              const double sr = (double)a.qsum[rhs];
-              const double uj = rd.u[j], vj = rd.v[j];
-              const double off = (double)rd.s1cnt[2 * j] - uj * (double)rd.s1cnt[2 * j + 1];
+              const double sc = s_q[3 * rhs], mean = s_q[3 * rhs + 1], sr = s_q[3 * rhs + 2];
+              const double uj = cu[rb], vj = cv[rb];
+              const double off = (double)cs1[rb] - uj * (double)ccn[rb];
               const double inner = (double)Tq + uj * ((double)Mq - sr);
               val = vj * (inner * sc + mean * off);
               rd.out[j] = a.scale_out * val;
