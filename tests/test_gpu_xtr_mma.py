@@ -44,7 +44,7 @@ def test_mma_single_rhs_matches_reference_kernel(n, p, miss):
     _check(m.aty_genetic(r, mode="mma"), ref.aty_genetic(r))
 
 
-@pytest.mark.parametrize("B", [1, 2, 3, 4, 5, 8, 9, 16, 17, 32, 33, 40])
+@pytest.mark.parametrize("B", [1, 2, 3, 4, 5, 8, 9, 12, 13, 16, 17, 20, 21, 32, 33, 40])
 @pytest.mark.parametrize("miss", [0.0, 0.02])
 def test_mma_batched_matches_per_rhs_reference(B, miss):
     n, p = 2500, 4000
