@@ -232,7 +232,7 @@ typedef struct {
 /* Replaces genoiht.fit (iht.py:326-354) on one GPU: the complete IHT loop with
  * device kernels, one host sync per phase.  y (n) and C (row-major n x c,
  * c <= 64) are host arrays over the handle's n samples; keep (n, optional)
- * restricts the fit to rows with keep == 1 (cross-validation training rows:
+ * restricts the fit to rows with keep != 0, 2 (cross-validation training rows:
  * other rows' residuals are pinned to 0); rows with keep == 2 are held out and
  * scored after the fit (heldout_sse / heldout_n: the fold's test rows,
  * model_select.py:138-139); u, v (p, optional) override the

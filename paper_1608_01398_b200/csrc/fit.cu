@@ -784,16 +784,18 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
   GI_CUDA_TRY(cudaMemcpyAsync(ws->y, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
   if (c) GI_CUDA_TRY(cudaMemcpyAsync(ws->C, C, sizeof(double) * n * c, cudaMemcpyHostToDevice, s));
   if (masked) {
-    // keep: 1 = a fit row, 2 = a held-out row scored after the fit, 0 = neither
+    // keep: 2 = a held-out row scored after the fit, other nonzero = a fit row,
+    // 0 = neither
     std::vector<uint8_t> fit_rows((size_t)n), test_rows((size_t)n);
     std::vector<uint32_t> mask((size_t)(ws->npad / 16), 0u);
     int64_t cnt = 0;
     n_test = 0;
     for (int64_t i = 0; i < n; ++i) {
-      fit_rows[(size_t)i] = keep[i] == 1;
+      const bool fit_row = keep[i] != 0 && keep[i] != 2;
+      fit_rows[(size_t)i] = fit_row;
       test_rows[(size_t)i] = keep[i] == 2;
       n_test += keep[i] == 2;
-      if (keep[i] == 1) {
+      if (fit_row) {
         mask[(size_t)(i >> 4)] |= 1u << (2 * (i & 15));
         ++cnt;
       }
