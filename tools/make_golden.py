@@ -197,6 +197,12 @@ def large_cases():
              path=np.arange(2, 12, 2), fold_seed=77, std_mode="train", warm=True),
         dict(name="cvL_global_warm_miss", n=2600, p=14000, seed=5252, missing=0.02, q=4,
              path=np.arange(2, 12, 2), fold_seed=77, std_mode="global", warm=True),
+        # cold starts with missing genotypes: the lock-step group's tensor-core
+        # sweeps with the missing-flag MMAs, and the base-3 copy + missing list
+        dict(name="cvL_train_cold_miss", n=2600, p=14000, seed=5353, missing=0.02, q=4,
+             path=np.arange(1, 9), fold_seed=91, std_mode="train", warm=False),
+        dict(name="cvL_global_cold_miss", n=2600, p=14000, seed=5353, missing=0.02, q=4,
+             path=np.arange(1, 9), fold_seed=91, std_mode="global", warm=False),
     ]
     for sp in cv_specs:
         m = _synth_matrix(sp["n"], sp["p"], sp["seed"], sp["missing"])
