@@ -432,7 +432,7 @@ class NativeFit {
                               &pub, ws_->ticket, ws_->dmap, ws_->aty_part, ws_->aty_ticket));
       if (ev1) GI_CUDA_TRY(cudaEventRecord(ev1, s));
       ++aty_launches;
-      ++launches;
+      launches += d.mlist != nullptr ? 2 : 1;  // + missum_kernel over the missing list
       if (ks > 0 && support_grad_) {
         TRY(gi::launch_support_grad(d, ws_->r, ws_->u, ws_->v, ws_->scal + 6, -1.0, d_sup, ks,
                                     ws_->g, ws_->dmap + ws_->oR + 8 + ws_->c, ws_->sg_part,
