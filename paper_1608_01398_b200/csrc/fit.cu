@@ -699,6 +699,15 @@ double dot(const std::vector<double>& a) {
   return s;
 }
 
+// GI_TRACE_FIT=2: one stderr line per iteration (restriction, gradients, mu)
+bool trace_steps() {
+  static const bool on = [] {
+    const char* e = getenv("GI_TRACE_FIT");
+    return e && e[0] == '2';
+  }();
+  return on;
+}
+
 bool any_nonzero(const std::vector<double>& a) {
   for (double x : a)
     if (x != 0.0) return true;
@@ -935,6 +944,12 @@ static int fit_impl(gi_matrix* h, gi_comm* comm, int64_t j_base, const double* y
           return -3;
         }
         double mu = den_mu[1];  // == num / den, computed on the device in IEEE fp64
+        if (trace_steps())
+          fprintf(stderr,
+                  "gi_fit step %lld: restriction %zu (g[0] %.17g), g_cov[0] %.17g, num %.17g, "
+                  "den %.17g, mu %.17g\n",
+                  (long long)it, ridx.size(), rg.empty() ? 0.0 : rg[0], c ? gcov[0] : 0.0, num,
+                  den, mu);
         bool accepted = false;
         int64_t bt = 0;
         for (int64_t tries = 0; tries <= cfg->max_backtracks; ++tries) {
