@@ -296,6 +296,23 @@ typedef struct gi_fit_job {
 } gi_fit_job;
 int gi_fit_many(gi_batch *batch, gi_fit_job *jobs, int64_t njobs, int threads);
 
+/* Replaces the fold x budget loop of genoiht.cv_iht (model_select.py:101-139)
+ * for cold starts: q folds (fold_labels[i] in 0..q-1 over the handle's n
+ * samples) x the npath budgets of path, every fit cold-started (covariate
+ * block by minimum-norm least squares on the fold's training rows, as
+ * numpy.linalg.lstsq, iht.py:208) on the fold's training rows -- std_mode 0:
+ * standardised with the training rows' statistics (model_select.py:87-93), 1:
+ * with the handle's -- and scored on the fold's test rows: mse[ki * q + f] =
+ * mean squared prediction error of budget path[ki] on fold f
+ * (model_select.py:138-139).  The fits run through gi_fit_many on `threads`
+ * native threads, in a lock-step group (shared tensor-core X^T R sweeps) when
+ * the fast kernel runs on more than 256 MB of genotypes.  select_k, the final
+ * fit and refit_least_squares stay with the caller (model_select.py:141-146).
+ * A failed fit returns its status with "solver failed at fold f, k=k: ...". */
+int gi_cv(gi_matrix *h, const double *y, const double *C, int64_t c, const int32_t *fold_labels,
+          int q, const int64_t *path, int64_t npath, const gi_fit_config *cfg, int std_mode,
+          int threads, double *mse);
+
 /* ------------------------------------------------ SNP-sharded native loop */
 /* One process per GPU, each holding a contiguous SNP block [j_base, j_base +
  * p_local) of the matrix.  The shards exchange only the

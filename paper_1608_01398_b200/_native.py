@@ -115,6 +115,8 @@ def _declare(lib):
         "gi_comm_free": ([P], c_int),
         "gi_matrix_with_masked_stats": ([P, P, P], c_int),
         "gi_fit_many": ([P, P, c_i64, c_int], c_int),
+        "gi_cv": ([P, P, P, c_i64, P, c_int, P, c_i64, ctypes.POINTER(FitConfig), c_int, c_int, P],
+                  c_int),
         "gi_batch_create": ([P, c_int, P], c_int),
         "gi_batch_stats": ([P, P, P], c_int),
         "gi_batch_free": ([P], c_int),

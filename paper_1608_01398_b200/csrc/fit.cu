@@ -18,6 +18,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <limits>
 #include <map>
 #include <atomic>
 #include <mutex>
@@ -1136,6 +1137,208 @@ extern "C" int gi_fit_many(gi_batch* batch, gi_fit_job* jobs, int64_t njobs, int
     gi_set_error("gi_fit_many: at least one job failed (see the jobs' status)");
     return -1;
   }
+  return 0;
+}
+
+// ------------------------------------------------------------------ gi_cv
+namespace {
+
+// Minimum-norm least squares of y on the columns of A (rows x c, row-major)
+// with numpy.linalg.lstsq's rank cutoff (rcond = eps * max(rows, c) times the
+// largest singular value): one-sided Jacobi SVD, x = V S^+ U^T y.  The cold
+// starts' covariate block (iht.py:208); c <= 64.
+void lstsq_min_norm(const std::vector<double>& A, int64_t rows, int64_t c,
+                    const std::vector<double>& y, double* x) {
+  std::vector<double> W(A);  // columns get rotated into U S
+  std::vector<double> V((size_t)(c * c), 0.0);
+  for (int64_t j = 0; j < c; ++j) V[(size_t)(j * c + j)] = 1.0;
+  auto col = [&](int64_t i, int64_t j) -> double& { return W[(size_t)(i * c + j)]; };
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int64_t a = 0; a < c; ++a)
+      for (int64_t b = a + 1; b < c; ++b) {
+        double alpha = 0.0, beta = 0.0, gamma = 0.0;
+        for (int64_t i = 0; i < rows; ++i) {
+          alpha += col(i, a) * col(i, a);
+          beta += col(i, b) * col(i, b);
+          gamma += col(i, a) * col(i, b);
+        }
+        if (gamma == 0.0 || std::fabs(gamma) <= 1e-15 * std::sqrt(alpha * beta)) continue;
+        off = std::max(off, std::fabs(gamma) / std::sqrt(alpha * beta));
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = cs * t;
+        for (int64_t i = 0; i < rows; ++i) {
+          const double wa = col(i, a), wb = col(i, b);
+          col(i, a) = cs * wa - sn * wb;
+          col(i, b) = sn * wa + cs * wb;
+        }
+        for (int64_t i = 0; i < c; ++i) {
+          const double va = V[(size_t)(i * c + a)], vb = V[(size_t)(i * c + b)];
+          V[(size_t)(i * c + a)] = cs * va - sn * vb;
+          V[(size_t)(i * c + b)] = sn * va + cs * vb;
+        }
+      }
+    if (off <= 1e-15) break;
+  }
+  std::vector<double> sv((size_t)c);
+  double smax = 0.0;
+  for (int64_t j = 0; j < c; ++j) {
+    double s2 = 0.0;
+    for (int64_t i = 0; i < rows; ++i) s2 += col(i, j) * col(i, j);
+    sv[(size_t)j] = std::sqrt(s2);
+    smax = std::max(smax, sv[(size_t)j]);
+  }
+  const double cut = std::numeric_limits<double>::epsilon() * (double)std::max(rows, c) * smax;
+  std::vector<double> coef((size_t)c, 0.0);  // S^+ U^T y, U_j = W_j / s_j
+  for (int64_t j = 0; j < c; ++j) {
+    const double s = sv[(size_t)j];
+    if (!(s > cut)) continue;
+    double uy = 0.0;
+    for (int64_t i = 0; i < rows; ++i) uy += col(i, j) * y[(size_t)i];
+    coef[(size_t)j] = uy / (s * s);
+  }
+  for (int64_t r = 0; r < c; ++r) {
+    double acc = 0.0;
+    for (int64_t j = 0; j < c; ++j) acc += V[(size_t)(r * c + j)] * coef[(size_t)j];
+    x[r] = acc;
+  }
+}
+
+// the native loop's X^T r choice on a fold's shape (NativeFit): the exact
+// kernel fits never join a lock-step group
+bool cv_exact_kernel(const gi_matrix* h, int64_t n_fit, int64_t k, int64_t c) {
+  const double tiles = (double)h->T * (double)h->G * GI_BLOCK_BYTES;
+  return tiles <= 2.0 * 1048576.0 ||
+         ((double)n_fit <= 8.0 * (double)(k + c + 1) && tiles <= 256.0 * 1048576.0);
+}
+
+}  // namespace
+
+extern "C" int gi_cv(gi_matrix* h, const double* y, const double* C, int64_t c,
+                     const int32_t* fold_labels, int q, const int64_t* path, int64_t npath,
+                     const gi_fit_config* cfg, int std_mode, int threads, double* mse) {
+  CHECK_ARG(h && y && fold_labels && path && cfg && mse, "NULL argument");
+  CHECK_ARG(q >= 2, "need at least two folds");
+  CHECK_ARG(npath >= 1, "empty model-size path");
+  CHECK_ARG(c >= 0 && c <= 64 && (c == 0 || C != nullptr), "covariates: 0..64 columns");
+  CHECK_ARG(std_mode == 0 || std_mode == 1, "std_mode: 0 = train, 1 = global");
+  CHECK_ARG(threads >= 1, "need at least one thread");
+  const int64_t n = h->n;
+  std::vector<int64_t> fold_size((size_t)q, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    CHECK_ARG(fold_labels[i] >= 0 && fold_labels[i] < q, "fold label out of range");
+    ++fold_size[(size_t)fold_labels[i]];
+  }
+  int64_t kmax = 0;
+  for (int64_t i = 0; i < npath; ++i) {
+    CHECK_ARG(path[i] >= 0, "negative budget");
+    kmax = std::max(kmax, path[i]);
+  }
+  const int64_t min_train = n - *std::max_element(fold_size.begin(), fold_size.end());
+  CHECK_ARG(kmax + c < min_train,
+            "largest budget plus covariates must stay below the smallest training fold");
+  // per fold: its row mask (1 training row, 2 test row), its matrix handle
+  // (train mode: statistics of the training rows, formed on the device) and
+  // the cold start's covariate block
+  std::vector<std::vector<uint8_t>> keep((size_t)q);
+  std::vector<gi_matrix*> fold_h((size_t)q, nullptr);
+  struct FoldHandles {
+    std::vector<gi_matrix*>& v;
+    gi_matrix* base;
+    ~FoldHandles() {
+      for (gi_matrix* m : v)
+        if (m && m != base) gi_matrix_free(m);
+    }
+  } fold_guard{fold_h, h};
+  std::vector<double> bcov0((size_t)(q * std::max<int64_t>(c, 1)), 0.0);
+  for (int f = 0; f < q; ++f) {
+    std::vector<uint8_t>& kf = keep[(size_t)f];
+    kf.resize((size_t)n);
+    std::vector<uint8_t> train((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      kf[(size_t)i] = fold_labels[i] == f ? 2 : 1;
+      train[(size_t)i] = fold_labels[i] != f;
+    }
+    if (std_mode == 0)
+      TRY(gi_matrix_with_masked_stats(h, train.data(), &fold_h[(size_t)f]));
+    else
+      fold_h[(size_t)f] = h;
+    if (c) {
+      const int64_t nt = n - fold_size[(size_t)f];
+      std::vector<double> A((size_t)(nt * c)), yt((size_t)nt);
+      int64_t r = 0;
+      for (int64_t i = 0; i < n; ++i)
+        if (train[(size_t)i]) {
+          for (int64_t l = 0; l < c; ++l) A[(size_t)(r * c + l)] = C[i * c + l];
+          yt[(size_t)r++] = y[i];
+        }
+      lstsq_min_norm(A, nt, c, yt, &bcov0[(size_t)(f * c)]);
+    }
+  }
+  // every (fold, budget) fit in one gi_fit_many, in a lock-step group when
+  // the fits would run the fast kernel on more than 256 MB of genotypes
+  const bool big = (double)h->p * (double)h->nb >= 256.0 * 1048576.0;
+  gi_batch* group = nullptr;
+  if (big && !cv_exact_kernel(h, min_train, kmax, c)) TRY(gi_batch_create(h, 0, &group));
+  struct GroupGuard {
+    gi_batch* g;
+    ~GroupGuard() {
+      if (g) gi_batch_free(g);
+    }
+  } group_guard{group};
+  const int64_t njobs = (int64_t)q * npath;
+  std::vector<gi_fit_config> cfgs((size_t)njobs, *cfg);
+  std::vector<gi_fit_result> res((size_t)njobs);
+  std::vector<int64_t> sup_buf, tr_buf;
+  std::vector<double> w_buf, cov_buf, trace_buf;
+  int64_t cap_total = 0;
+  for (int64_t i = 0; i < npath; ++i) cap_total += std::max<int64_t>(path[i], 1);
+  sup_buf.resize((size_t)(q * cap_total));
+  w_buf.resize((size_t)(q * cap_total));
+  cov_buf.resize((size_t)(njobs * std::max<int64_t>(c, 1)));
+  trace_buf.resize((size_t)(njobs * (cfg->max_iter + 1)));
+  std::vector<gi_fit_job> jobs((size_t)njobs);
+  int64_t off = 0;
+  for (int f = 0; f < q; ++f)
+    for (int64_t ki = 0; ki < npath; ++ki) {
+      const int64_t j = f * npath + ki, cap = std::max<int64_t>(path[ki], 1);
+      cfgs[(size_t)j].k = path[ki];
+      gi_fit_result& r = res[(size_t)j];
+      memset(&r, 0, sizeof(r));
+      r.support = sup_buf.data() + off;
+      r.weights = w_buf.data() + off;
+      r.support_cap = cap;
+      r.covar = cov_buf.data() + j * std::max<int64_t>(c, 1);
+      r.loss_trace = trace_buf.data() + j * (cfg->max_iter + 1);
+      r.trace_cap = cfg->max_iter + 1;
+      off += cap;
+      gi_fit_job& jb = jobs[(size_t)j];
+      memset(&jb, 0, sizeof(jb));
+      jb.h = fold_h[(size_t)f];
+      jb.y = y;
+      jb.C = C;
+      jb.c = c;
+      jb.keep = keep[(size_t)f].data();
+      jb.cfg = &cfgs[(size_t)j];
+      jb.bcov0 = c ? &bcov0[(size_t)(f * c)] : nullptr;
+      jb.res = &r;
+    }
+  const int rc = gi_fit_many(group, jobs.data(), njobs, threads);
+  if (rc != 0) {
+    for (int64_t j = 0; j < njobs; ++j)
+      if (jobs[(size_t)j].status != 0) {
+        gi_set_error("solver failed at fold %lld, k=%lld: %s", (long long)(j / npath),
+                     (long long)path[j % npath], jobs[(size_t)j].error);
+        return jobs[(size_t)j].status;
+      }
+    return rc;
+  }
+  for (int f = 0; f < q; ++f)
+    for (int64_t ki = 0; ki < npath; ++ki) {
+      const gi_fit_result& r = res[(size_t)(f * npath + ki)];
+      mse[ki * q + f] = r.heldout_n > 0 ? r.heldout_sse / (double)r.heldout_n : 0.0;
+    }
   return 0;
 }
 

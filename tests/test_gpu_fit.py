@@ -312,3 +312,30 @@ def test_fit_many_matches_single_fits_and_reports_per_job_errors():
         np.testing.assert_array_equal(res.model.support, want.model.support)
         np.testing.assert_array_equal(res.model.weights, want.model.weights)
         assert res.iterations == want.iterations
+
+
+@pytest.mark.parametrize("std_mode,ncov", [("train", 0), ("global", 2), ("train", 2)])
+def test_gi_cv_grid_equals_cv_iht(std_mode, ncov):
+    """gi_cv (model_select.cv_mse): the whole cold-start fold x budget loop in
+    one C-ABI call gives cv_iht's MSE grid (same fits; the covariate least
+    squares rounds differently, hence 1e-9) and reports failing fits like the
+    reference."""
+    gi = _gi()
+    from paper_1608_01398_b200.model_select import cv_mse
+
+    n, p = 900, 2500
+    codes = oracle.random_codes(n, p, seed=61, missing_rate=0.02)
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    rng = np.random.default_rng(6)
+    raw = rng.standard_normal((n, ncov)) if ncov else None
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(raw, n=n))
+    support = np.sort(rng.choice(p, 5, replace=False))
+    y = m.ax_columns(support, rng.standard_normal(5)) + rng.normal(0, 0.4, n)
+    plan = gi.CvPlan.build(n, 4, np.arange(1, 9), seed=13)
+    grid = cv_mse(view, y, plan, gi.IhtConfig(k=8), std_mode=std_mode)
+    rep = gi.cv_iht(view, y, plan, gi.IhtConfig(k=8), std_mode=std_mode)
+    np.testing.assert_allclose(grid, rep.mse, rtol=1e-9)
+    bad = y.copy()
+    bad[5] = np.inf
+    with pytest.raises(Exception, match="fold"):
+        cv_mse(view, bad, plan, gi.IhtConfig(k=8), std_mode=std_mode)
