@@ -273,7 +273,8 @@ int gi_fit_batched(gi_matrix *h, gi_batch *batch, const double *y, const double 
  * gi_fit_batched (batch != NULL) with job i's arguments, run on `threads`
  * native worker threads that take the jobs in index order.  Each job's
  * status (0 or a gi_fit error code) and error message land in the job; the
- * call returns 0 when every job succeeded, -1 otherwise.  Host threads of
+ * call returns 0 when every job succeeded, -1 otherwise.  Chains of jobs
+ * (warm_from) give the warm-started budget path of cv_iht (model_select.py:131-137).  Host threads of
  * the caller's language (and its interpreter lock) stay out of the fits'
  * start-up: a Python thread pool needed ~1 ms per job to hand 32 fits their
  * threads. */
@@ -291,27 +292,33 @@ typedef struct gi_fit_job {
   int64_t warm_k;
   const double *bcov0;
   gi_fit_result *res;
+  int64_t warm_from; /* -1, or an earlier job whose result warm-starts this one
+                        (trimmed to cfg->k as initial_state does); the job then
+                        runs on that job's thread right after it, and
+                        warm_idx / warm_w / warm_k / bcov0 are ignored */
   int status;       /* out */
   char error[256];  /* out: gi_last_error() of a failed job */
 } gi_fit_job;
 int gi_fit_many(gi_batch *batch, gi_fit_job *jobs, int64_t njobs, int threads);
 
-/* Replaces the fold x budget loop of genoiht.cv_iht (model_select.py:101-139)
- * for cold starts: q folds (fold_labels[i] in 0..q-1 over the handle's n
- * samples) x the npath budgets of path, every fit cold-started (covariate
- * block by minimum-norm least squares on the fold's training rows, as
- * numpy.linalg.lstsq, iht.py:208) on the fold's training rows -- std_mode 0:
+/* Replaces the fold x budget loop of genoiht.cv_iht (model_select.py:101-139):
+ * q folds (fold_labels[i] in 0..q-1 over the handle's n samples) x the npath
+ * budgets of path, each fit cold-started (covariate block by minimum-norm
+ * least squares on the fold's training rows, as numpy.linalg.lstsq,
+ * iht.py:208) or, with warm_start, from the fold's previous budget
+ * (model_select.py:131-137), on the fold's training rows -- std_mode 0:
  * standardised with the training rows' statistics (model_select.py:87-93), 1:
  * with the handle's -- and scored on the fold's test rows: mse[ki * q + f] =
  * mean squared prediction error of budget path[ki] on fold f
  * (model_select.py:138-139).  The fits run through gi_fit_many on `threads`
- * native threads, in a lock-step group (shared tensor-core X^T R sweeps) when
- * the fast kernel runs on more than 256 MB of genotypes.  select_k, the final
+ * native threads, cold starts in a lock-step group (shared tensor-core X^T R
+ * sweeps) when the fast kernel runs on more than 256 MB of genotypes, warm
+ * starts as one chain per fold.  select_k, the final
  * fit and refit_least_squares stay with the caller (model_select.py:141-146).
  * A failed fit returns its status with "solver failed at fold f, k=k: ...". */
 int gi_cv(gi_matrix *h, const double *y, const double *C, int64_t c, const int32_t *fold_labels,
           int q, const int64_t *path, int64_t npath, const gi_fit_config *cfg, int std_mode,
-          int threads, double *mse);
+          int warm_start, int threads, double *mse);
 
 /* ------------------------------------------------ SNP-sharded native loop */
 /* One process per GPU, each holding a contiguous SNP block [j_base, j_base +

@@ -57,7 +57,7 @@ class FitJob(ctypes.Structure):
     _fields_ = [("h", c_vp), ("y", c_vp), ("C", c_vp), ("c", c_i64), ("keep", c_vp),
                 ("u", c_vp), ("v", c_vp), ("cfg", ctypes.POINTER(FitConfig)),
                 ("warm_idx", c_vp), ("warm_w", c_vp), ("warm_k", c_i64), ("bcov0", c_vp),
-                ("res", ctypes.POINTER(FitOut)), ("status", c_int),
+                ("res", ctypes.POINTER(FitOut)), ("warm_from", c_i64), ("status", c_int),
                 ("error", ctypes.c_char * 256)]
 
 
@@ -115,7 +115,8 @@ def _declare(lib):
         "gi_comm_free": ([P], c_int),
         "gi_matrix_with_masked_stats": ([P, P, P], c_int),
         "gi_fit_many": ([P, P, c_i64, c_int], c_int),
-        "gi_cv": ([P, P, P, c_i64, P, c_int, P, c_i64, ctypes.POINTER(FitConfig), c_int, c_int, P],
+        "gi_cv": ([P, P, P, c_i64, P, c_int, P, c_i64, ctypes.POINTER(FitConfig), c_int, c_int,
+                   c_int, P],
                   c_int),
         "gi_batch_create": ([P, c_int, P], c_int),
         "gi_batch_stats": ([P, P, P], c_int),

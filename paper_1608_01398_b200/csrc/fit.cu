@@ -1112,22 +1112,82 @@ extern "C" int gi_fit_batched(gi_matrix* h, gi_batch* batch, const double* y, co
 extern "C" int gi_fit_many(gi_batch* batch, gi_fit_job* jobs, int64_t njobs, int threads) {
   CHECK_ARG(njobs >= 0 && (njobs == 0 || jobs != nullptr), "invalid job list");
   CHECK_ARG(threads >= 1, "need at least one thread");
+  // chains: a job with warm_from = i starts from job i's result, on the thread
+  // that ran job i, right after it (cv_iht's warm-started budget path)
+  std::vector<int64_t> succ((size_t)njobs, -1), heads;
+  for (int64_t i = 0; i < njobs; ++i) {
+    const int64_t w = jobs[i].warm_from;
+    if (w < 0) {
+      heads.push_back(i);
+      continue;
+    }
+    CHECK_ARG(w < i, "warm_from must name an earlier job");
+    CHECK_ARG(succ[(size_t)w] < 0, "a job warm-starts at most one other job");
+    CHECK_ARG(jobs[i].warm_idx == nullptr && jobs[i].warm_k == 0,
+              "a chained job takes its warm start from warm_from only");
+    succ[(size_t)w] = i;
+  }
   std::atomic<int64_t> next{0};
   std::atomic<int> failed{0};
+  const int64_t nheads = (int64_t)heads.size();
+  auto run = [&](gi_fit_job& j, const int64_t* widx, const double* ww, int64_t wk,
+                 const double* b0) {
+    const int rc = fit_impl(j.h, nullptr, 0, j.y, j.C, j.c, j.keep, j.u, j.v, j.cfg, widx, ww,
+                            wk, b0, j.res, batch);
+    j.status = rc;
+    j.error[0] = '\0';
+    if (rc != 0) {
+      snprintf(j.error, sizeof(j.error), "%s", gi_last_error());
+      failed.store(1);
+    }
+    return rc;
+  };
   auto worker = [&]() {
-    for (int64_t i = next.fetch_add(1); i < njobs; i = next.fetch_add(1)) {
-      gi_fit_job& j = jobs[i];
-      const int rc = fit_impl(j.h, nullptr, 0, j.y, j.C, j.c, j.keep, j.u, j.v, j.cfg, j.warm_idx,
-                              j.warm_w, j.warm_k, j.bcov0, j.res, batch);
-      j.status = rc;
-      j.error[0] = '\0';
-      if (rc != 0) {
-        snprintf(j.error, sizeof(j.error), "%s", gi_last_error());
-        failed.store(1);
+    std::vector<int64_t> widx;
+    std::vector<double> ww, wb;
+    for (int64_t hi = next.fetch_add(1); hi < nheads; hi = next.fetch_add(1)) {
+      int64_t i = heads[(size_t)hi];
+      int rc = run(jobs[i], jobs[i].warm_idx, jobs[i].warm_w, jobs[i].warm_k, jobs[i].bcov0);
+      for (int64_t nx = succ[(size_t)i]; nx >= 0; i = nx, nx = succ[(size_t)nx]) {
+        gi_fit_job& jn = jobs[nx];
+        if (rc != 0) {  // the chain stops at a failed fit (the reference's loop raises there)
+          jn.status = rc;
+          snprintf(jn.error, sizeof(jn.error), "warm start source (job %lld) failed",
+                   (long long)i);
+          failed.store(1);
+          continue;
+        }
+        // the previous result, trimmed to this budget by |weight| with ties to
+        // the lower index (initial_state's hard_threshold, iht.py:204-206)
+        const gi_fit_result& pr = *jobs[i].res;
+        widx.assign(pr.support, pr.support + pr.nnz);
+        ww.assign(pr.weights, pr.weights + pr.nnz);
+        const int64_t k = jn.cfg->k;
+        if ((int64_t)widx.size() > k) {
+          std::vector<int64_t> ord(widx.size());
+          for (size_t t = 0; t < ord.size(); ++t) ord[t] = (int64_t)t;
+          std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+            const double fa = std::fabs(ww[(size_t)a]), fb = std::fabs(ww[(size_t)b]);
+            return fa != fb ? fa > fb : widx[(size_t)a] < widx[(size_t)b];
+          });
+          ord.resize((size_t)k);
+          std::sort(ord.begin(), ord.end());
+          std::vector<int64_t> ti;
+          std::vector<double> tw;
+          for (int64_t t : ord) {
+            ti.push_back(widx[(size_t)t]);
+            tw.push_back(ww[(size_t)t]);
+          }
+          widx.swap(ti);
+          ww.swap(tw);
+        }
+        wb.assign(pr.covar, pr.covar + jn.c);
+        rc = run(jn, widx.empty() ? nullptr : widx.data(), ww.empty() ? nullptr : ww.data(),
+                 (int64_t)widx.size(), wb.data());
       }
     }
   };
-  const int nt = (int)std::min<int64_t>(threads, std::max<int64_t>(njobs, 1));
+  const int nt = (int)std::min<int64_t>(threads, std::max<int64_t>(nheads, 1));
   std::vector<std::thread> pool;
   pool.reserve((size_t)nt);
   for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
@@ -1217,7 +1277,8 @@ bool cv_exact_kernel(const gi_matrix* h, int64_t n_fit, int64_t k, int64_t c) {
 
 extern "C" int gi_cv(gi_matrix* h, const double* y, const double* C, int64_t c,
                      const int32_t* fold_labels, int q, const int64_t* path, int64_t npath,
-                     const gi_fit_config* cfg, int std_mode, int threads, double* mse) {
+                     const gi_fit_config* cfg, int std_mode, int warm_start, int threads,
+                     double* mse) {
   CHECK_ARG(h && y && fold_labels && path && cfg && mse, "NULL argument");
   CHECK_ARG(q >= 2, "need at least two folds");
   CHECK_ARG(npath >= 1, "empty model-size path");
@@ -1280,7 +1341,8 @@ extern "C" int gi_cv(gi_matrix* h, const double* y, const double* C, int64_t c,
   // the fits would run the fast kernel on more than 256 MB of genotypes
   const bool big = (double)h->p * (double)h->nb >= 256.0 * 1048576.0;
   gi_batch* group = nullptr;
-  if (big && !cv_exact_kernel(h, min_train, kmax, c)) TRY(gi_batch_create(h, 0, &group));
+  if (big && !warm_start && !cv_exact_kernel(h, min_train, kmax, c))
+    TRY(gi_batch_create(h, 0, &group));
   struct GroupGuard {
     gi_batch* g;
     ~GroupGuard() {
@@ -1315,6 +1377,8 @@ extern "C" int gi_cv(gi_matrix* h, const double* y, const double* C, int64_t c,
       off += cap;
       gi_fit_job& jb = jobs[(size_t)j];
       memset(&jb, 0, sizeof(jb));
+      // warm starts: each budget from the fold's previous one (model_select.py:131-137)
+      jb.warm_from = warm_start && ki > 0 ? j - 1 : -1;
       jb.h = fold_h[(size_t)f];
       jb.y = y;
       jb.C = C;
