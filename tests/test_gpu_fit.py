@@ -344,3 +344,28 @@ def test_gi_cv_grid_equals_cv_iht(std_mode, ncov, warm):
     bad[5] = np.inf
     with pytest.raises(Exception, match="fold"):
         cv_mse(view, bad, plan, gi.IhtConfig(k=8), std_mode=std_mode)
+
+
+def test_fit_path_warm_chain_equals_sequential_warm_fits():
+    """fit_path(warm_start=True) runs the budgets as one native chain
+    (gi_fit_job.warm_from): the same bits as fit() called budget by budget
+    with the previous model as the warm start (including budgets below the
+    previous support: trimmed by |weight|, ties to the lower index)."""
+    gi = _gi()
+    n, p = 1200, 4000
+    codes = oracle.random_codes(n, p, seed=71, missing_rate=0.01)
+    m = gi.PackedGenotypeMatrix.from_codes(codes)
+    rng = np.random.default_rng(71)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(rng.standard_normal((n, 1)), n=n))
+    support = np.sort(rng.choice(p, 8, replace=False))
+    y = m.ax_columns(support, rng.standard_normal(8)) + rng.normal(0, 0.3, n)
+    path = [3, 6, 10, 4, 12]
+    got = gi.fit_path(view, y, path, warm_start=True)
+    warm = None
+    for k, res in zip(path, got):
+        want = gi.fit(view, y, gi.IhtConfig(k=k), warm=warm)
+        np.testing.assert_array_equal(res.model.support, want.model.support)
+        np.testing.assert_array_equal(res.model.weights, want.model.weights)
+        np.testing.assert_array_equal(res.model.covar, want.model.covar)
+        assert res.iterations == want.iterations
+        warm = want.model
