@@ -369,3 +369,24 @@ def test_fit_path_warm_chain_equals_sequential_warm_fits():
         np.testing.assert_array_equal(res.model.covar, want.model.covar)
         assert res.iterations == want.iterations
         warm = want.model
+
+
+def test_gi_cv_lockstep_group_matches_cv_iht():
+    """gi_cv above 256 MB of genotypes forms its lock-step group itself (the
+    fits' X^T r sweeps on the tensor cores): the same grid as cv_iht's own
+    group, and both far from trivial (several residuals per sweep)."""
+    gi = _gi()
+    from paper_1608_01398_b200.model_select import LAST_BATCH, cv_mse
+
+    n, p = 20000, 60000  # 300 MB of 2-bit tiles
+    m = gi.PackedGenotypeMatrix.synthetic(n, p, 77)
+    view = gi.StandardizedView(m, gi.CovariateBlock.build(None, n=n))
+    rng = np.random.default_rng(77)
+    support = np.sort(rng.choice(p, 6, replace=False))
+    y = m.ax_columns(support, rng.standard_normal(6)) + rng.normal(0, 0.5, n)
+    plan = gi.CvPlan.build(n, 3, np.arange(1, 5), seed=5)
+    LAST_BATCH.clear()
+    rep = gi.cv_iht(view, y, plan, gi.IhtConfig(k=4))
+    assert LAST_BATCH.get("sweeps", 0) > 0 and LAST_BATCH["rhs"] >= 2 * LAST_BATCH["sweeps"]
+    grid = cv_mse(view, y, plan, gi.IhtConfig(k=4))
+    np.testing.assert_allclose(grid, rep.mse, rtol=1e-9)
